@@ -1,0 +1,117 @@
+/*
+ * toesplit_ext.h — additive B200 extensions to the toesplit C ABI.
+ *
+ * Nothing here changes toesplit.h (the reference ABI, ref
+ * proj/include/toesplit.h); these are new symbols for what BASELINE.json's
+ * configs need and the reference lacks (SURVEY.md §0 "gaps", §8(b)):
+ *   - complex64 operators (complex128 remains the default),
+ *   - m x m blocks (e.g. 3x3 dyadic Green tensors) with a unique-component
+ *     map, so a block-symmetric G stores 6 of its 9 components,
+ *   - per-axis symmetry signs, generalising ref generator.hpp:9's single mode
+ *     (the off-diagonal dyadic G_ij is odd along axes i and j, even along the
+ *     third),
+ *   - device-pointer apply on a caller stream (no PCIe in the loop),
+ *   - branch partitions: an operator that owns the subtree of branch ids whose
+ *     low q bits equal `part` (nparts = 2^q) and returns that subtree's
+ *     projected partial output; summing the partials over parts (an NCCL
+ *     reduce across GPUs) gives y (paper outlook).
+ *
+ * Vector layout for m-component operators: m component tensors back to back
+ * (SoA), each prod(levels) complex elements, row-major, level 1 outermost.
+ * ts_operator_apply on an m-component operator reads/writes m*prod(levels)
+ * interleaved complex doubles in that layout.
+ */
+#ifndef TOESPLIT_EXT_H
+#define TOESPLIT_EXT_H
+
+#include "toesplit.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ts_precision {
+    TS_PREC_C128 = 0, /* complex<double>, the reference's only precision */
+    TS_PREC_C64 = 1   /* complex<float> storage and arithmetic; spectra and
+                         twiddles are computed in double and rounded */
+} ts_precision;
+
+typedef struct ts_block_generator ts_block_generator;
+
+/* Explicit m x m block generator. comp_map[i*m+j] in [0, n_unique) names the
+ * unique component used at block position (i, j); lags[u] is that component's
+ * interleaved lag tensor (as ts_generator_create); axis_sign[u*d + a] is +1
+ * (t_m == t_{-m} under negation of lag a), -1 (t_m == -t_{-m}) or 0 (no
+ * symmetry), validated exactly like ref generator.cpp:38-62. */
+ts_status ts_block_generator_create(int32_t d, const int64_t* levels, int32_t m,
+                                    int32_t n_unique, const int32_t* comp_map,
+                                    const double* const* lags, const int32_t* axis_sign,
+                                    ts_block_generator** out);
+
+/* The synthetic dyadic Green kernel of BASELINE.json configs[1..3] (d = 3,
+ * m = 3, 6 unique components, per-axis parity (-1)^([i=a]+[j=a])):
+ * G_ij(r) = (d_ij - rh_i rh_j) e^{ikr}/r + (d_ij - 3 rh_i rh_j) e^{ikr}/(k^2 r^3),
+ * G(0) = (self_re + i self_im) I, on unit-spaced integer offsets. Lags are
+ * evaluated analytically on the device at operator creation (never
+ * materialised on the host). */
+ts_status ts_block_generator_dyadic(int32_t d, const int64_t* levels, double k, double self_re,
+                                    double self_im, ts_block_generator** out);
+
+/* Wrap a scalar generator (m = 1); per-axis signs from its symmetry mode. */
+ts_status ts_block_generator_from_scalar(const ts_generator* g, ts_block_generator** out);
+
+int32_t ts_block_generator_components(const ts_block_generator* g);
+void ts_block_generator_destroy(ts_block_generator* g);
+
+typedef struct ts_split_options {
+    int32_t precision; /* ts_precision */
+    int32_t storage;   /* ts_storage */
+    int32_t device;    /* CUDA ordinal, -1 = current */
+    int32_t part;      /* owned branch subtree, 0 <= part < nparts */
+    int32_t nparts;    /* 1, 2, 4, ... <= 2^d */
+    double s0_re;      /* circulant padding value (result never depends on it) */
+    double s0_im;
+} ts_split_options;
+
+/* Fill *opt with defaults: c128, AUTO, current device, part 0 of 1, s0 = 0. */
+void ts_split_options_default(ts_split_options* opt);
+
+ts_status ts_operator_create_split_ex(const ts_block_generator* g, const ts_split_options* opt,
+                                      ts_operator** out);
+
+/* y = T x on device memory: x, y hold m components of prod(levels) elements of
+ * the operator's precision (float2 / double2), may not alias; stream is a
+ * cudaStream_t (NULL = legacy default stream). Asynchronous: returns after
+ * enqueueing; metrics (nullable) carries counters, apply_ns = 0. Workspace is
+ * stream-ordered per call, so concurrent calls on different streams are safe.
+ * For a partition operator y receives the partial output of its subtree. */
+ts_status ts_operator_apply_device(const ts_operator* op, const void* x, void* y, void* stream,
+                                   ts_metrics* metrics);
+
+typedef struct ts_operator_info {
+    int32_t d;
+    int32_t m;          /* vector components / block arity */
+    int32_t n_unique;   /* stored components */
+    int32_t precision;  /* ts_precision */
+    int32_t storage;    /* resolved ts_storage (FULL or COMPRESSED) */
+    int32_t is_embed;   /* 1 for full-embedding baseline operators */
+    int32_t device;
+    int32_t part;
+    int32_t nparts;
+    int32_t reserved;
+    uint64_t elem_bytes;       /* 8 (c64) or 16 (c128) */
+    uint64_t spectra_bytes;    /* device bytes of stored spectra */
+    uint64_t workspace_bytes;  /* device working set of one apply_device call */
+    uint64_t launches;         /* kernels per apply_device call */
+} ts_operator_info;
+
+ts_status ts_operator_get_info(const ts_operator* op, ts_operator_info* out);
+
+/* Number of visible CUDA devices (0 when none); never fails. */
+int32_t ts_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TOESPLIT_EXT_H */

@@ -1,0 +1,189 @@
+// Shared device helpers for the toesplit sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "tsk_launch.h"
+
+namespace tsk {
+
+template <typename T>
+struct cx;
+template <>
+struct cx<float> {
+    using t = float2;
+};
+template <>
+struct cx<double> {
+    using t = double2;
+};
+
+template <typename T>
+__device__ __forceinline__ typename cx<T>::t make_c(T x, T y)
+{
+    typename cx<T>::t r;
+    r.x = x;
+    r.y = y;
+    return r;
+}
+
+template <typename T2>
+__device__ __forceinline__ T2 cadd(T2 a, T2 b)
+{
+    T2 r;
+    r.x = a.x + b.x;
+    r.y = a.y + b.y;
+    return r;
+}
+
+template <typename T2>
+__device__ __forceinline__ T2 csub(T2 a, T2 b)
+{
+    T2 r;
+    r.x = a.x - b.x;
+    r.y = a.y - b.y;
+    return r;
+}
+
+// (a.x + i a.y)(b.x + i b.y)
+template <typename T2>
+__device__ __forceinline__ T2 cmul(T2 a, T2 b)
+{
+    T2 r;
+    r.x = a.x * b.x - a.y * b.y;
+    r.y = a.x * b.y + a.y * b.x;
+    return r;
+}
+
+// a * conj(b)
+template <typename T2>
+__device__ __forceinline__ T2 cmulc(T2 a, T2 b)
+{
+    T2 r;
+    r.x = a.x * b.x + a.y * b.y;
+    r.y = a.y * b.x - a.x * b.y;
+    return r;
+}
+
+__device__ __forceinline__ float2 ldg_c(const float2* p) { return __ldg(p); }
+__device__ __forceinline__ double2 ldg_c(const double2* p) { return __ldg(p); }
+
+// Root table entry k (exp(-2 pi i k/n)); conjugated for inverse transforms.
+template <typename T, bool INV>
+__device__ __forceinline__ typename cx<T>::t twiddle(const typename cx<T>::t* __restrict__ roots,
+                                                     int k)
+{
+    typename cx<T>::t w = ldg_c(roots + k);
+    if (INV)
+        w.y = -w.y;
+    return w;
+}
+
+// multiply by -i (forward) or +i (inverse)
+template <typename T2, bool INV>
+__device__ __forceinline__ T2 mul_mi(T2 a)
+{
+    T2 r;
+    if (INV) {
+        r.x = -a.y;
+        r.y = a.x;
+    } else {
+        r.x = a.y;
+        r.y = -a.x;
+    }
+    return r;
+}
+
+template <typename T, bool INV>
+__device__ __forceinline__ void dft4(typename cx<T>::t& x0, typename cx<T>::t& x1,
+                                     typename cx<T>::t& x2, typename cx<T>::t& x3)
+{
+    using T2 = typename cx<T>::t;
+    const T2 s0 = cadd(x0, x2), d0 = csub(x0, x2);
+    const T2 s1 = cadd(x1, x3), d1 = mul_mi<T2, INV>(csub(x1, x3));
+    x0 = cadd(s0, s1);
+    x2 = csub(s0, s1);
+    x1 = cadd(d0, d1);
+    x3 = csub(d0, d1);
+}
+
+// In-register DFT of size R: v[q] <- sum_r v[r] w_R^{rq}, w_R = exp(-+2 pi i/R).
+// roots/m give w_R^e = roots[e*m] for the generic odd radices.
+template <typename T, int R, bool INV>
+__device__ __forceinline__ void dft_small(typename cx<T>::t* v,
+                                          const typename cx<T>::t* __restrict__ roots, int m)
+{
+    using T2 = typename cx<T>::t;
+    if constexpr (R == 2) {
+        const T2 a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    } else if constexpr (R == 4) {
+        dft4<T, INV>(v[0], v[1], v[2], v[3]);
+    } else if constexpr (R == 8) {
+        T2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+        T2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+        dft4<T, INV>(e0, e1, e2, e3);
+        dft4<T, INV>(o0, o1, o2, o3);
+        const T h = (T)0.70710678118654752440084436210484903928;
+        // o_q *= w8^q
+        {
+            T2 t;
+            t.x = h * (o1.x + (INV ? -o1.y : o1.y));
+            t.y = h * (o1.y + (INV ? o1.x : -o1.x));
+            o1 = t;
+        }
+        o2 = mul_mi<T2, INV>(o2);
+        {
+            T2 t;
+            t.x = h * (-o3.x + (INV ? -o3.y : o3.y));
+            t.y = h * (-o3.y + (INV ? o3.x : -o3.x));
+            o3 = t;
+        }
+        v[0] = cadd(e0, o0);
+        v[4] = csub(e0, o0);
+        v[1] = cadd(e1, o1);
+        v[5] = csub(e1, o1);
+        v[2] = cadd(e2, o2);
+        v[6] = csub(e2, o2);
+        v[3] = cadd(e3, o3);
+        v[7] = csub(e3, o3);
+    } else {
+        T2 out[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            T2 acc = v[0];
+#pragma unroll
+            for (int r = 1; r < R; ++r)
+                acc = cadd(acc, cmul(v[r], twiddle<T, INV>(roots, ((r * q) % R) * m)));
+            out[q] = acc;
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+            v[q] = out[q];
+    }
+}
+
+// ref kernel.cpp:17-21
+__host__ __device__ __forceinline__ int64_t stored_len(int64_t n, int odd)
+{
+    return odd ? (n + 1) / 2 : n / 2 + 1;
+}
+
+// ref kernel.cpp:25-37
+__host__ __device__ __forceinline__ int64_t mirror_src(int64_t n, int odd, int64_t k,
+                                                       bool& mirrored)
+{
+    if (odd) {
+        const int64_t st = (n + 1) / 2;
+        mirrored = k >= st;
+        return mirrored ? n - 1 - k : k;
+    }
+    mirrored = k > n / 2;
+    return mirrored ? n - k : k;
+}
+
+}  // namespace tsk

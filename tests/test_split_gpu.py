@@ -1,0 +1,263 @@
+"""GPU parity tests: the sm_100a split engine (through the C ABI) against the
+CPU oracle (oracle/, a restatement of the reference pinned to the reference
+build) and the reference's own known answers. Tolerances follow BASELINE.json:
+rel-L2 <= 1e-12 for complex128, <= 1e-5 for complex64, both against the
+complex128 oracle; the reference's own max-rel bars (1e-10 vs the dense
+product, 1e-12 vs the embedding engine, proj/tests/unit/test_engine_split.cpp)
+are kept where the reference asserts them.
+"""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2406_17981_b200 as T
+from oracle import max_rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+O = oracle.Oracle()
+SYM = [T.SYM_GENERAL, T.SYM_SYMMETRIC, T.SYM_SKEW]
+
+
+def _oracle_split(levels, sym, seed, variance=1.0, s0=0j, storage=-1):
+    lags = O.random_lags(levels, seed, variance, sym)
+    v = O.random_vector(levels, seed, variance)
+    signs = oracle.axis_signs(len(levels), sym)
+    comp = (sym == T.SYM_SYMMETRIC or (sym == T.SYM_SKEW and s0 == 0)) if storage == -1 else storage == 1
+    blocks = O.precompute(levels, lags, s0, comp, signs)
+    return lags, v, O.split_apply(levels, blocks, v, comp, signs)
+
+
+def test_worked_2x2_through_c_abi():
+    # ref tests/capi/test_capi.cpp:34-62 and tests/unit/test_engine_split.cpp:27-39
+    g = T.Generator.create([2], np.array([2, 1, 3], np.complex128))
+    op = T.Operator.split(g)
+    y, m = op.apply(np.array([1, 1], np.complex128), metrics=True)
+    assert abs(y[0] - 3) <= 1e-12 and abs(y[1] - 4) <= 1e-12
+    assert m["fft_forward"] == 2 and m["fft_inverse"] == 2
+    assert m["diag_mults"] == 4 and m["phase_mults"] == 4
+    assert m["peak_live_elems"] == 4
+
+
+@pytest.mark.parametrize("levels", [[2], [5], [3, 4], [2, 6], [2, 3, 4], [3, 3, 3]])
+@pytest.mark.parametrize("sym", SYM)
+def test_random_instances_vs_oracle_and_dense(levels, sym):
+    # ref tests/unit/test_engine_split.cpp:118-138
+    for seed in (1, 2, 3):
+        g = T.Generator.random(levels, seed, 1.0, sym)
+        lags, v, y_or = _oracle_split(levels, sym, seed)
+        y = T.Operator.split(g).apply(v)
+        y_naive = O.naive(levels, lags, v)
+        assert max_rel(y, y_naive) <= 1e-10
+        assert max_rel(y, y_or) <= 1e-12
+        assert rel_l2(y, y_or) <= 1e-12
+        y_emb = T.Operator.embed(g).apply(v)
+        assert max_rel(y_emb, y_naive) <= 1e-10
+        assert max_rel(y, y_emb) <= 1e-12
+
+
+@pytest.mark.parametrize("levels", [[13], [7, 5], [11, 2], [3, 5, 7], [9, 6, 4], [1, 4], [2, 1, 3]])
+def test_mixed_radix_and_prime_lengths(levels):
+    for sym in SYM:
+        g = T.Generator.random(levels, 5, 1.0, sym)
+        lags, v, y_or = _oracle_split(levels, sym, 5)
+        y = T.Operator.split(g).apply(v)
+        assert rel_l2(y, y_or) <= 1e-12
+        if np.prod(levels) <= 4096:
+            assert max_rel(y, O.naive(levels, lags, v)) <= 1e-10
+
+
+def test_c0_golden_16cubed_c128():
+    # BASELINE.json configs[0]: lags seed 0, x seed 1, variance 0.5 (CN(0,1))
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "c0_16cubed.npz"))
+    levels = [16, 16, 16]
+    g = T.Generator.random(levels, 0, 0.5, T.SYM_GENERAL)
+    x = T.random_vector(levels, 1, 0.5)
+    assert np.array_equal(x, gold["x"])
+    y = T.Operator.split(g).apply(x)
+    assert rel_l2(y, gold["y_split_ref"]) <= 1e-12
+    assert max_rel(y, gold["y_naive_ref"]) <= 1e-10
+    assert rel_l2(y, gold["y_naive_ref"]) <= 1e-12
+
+
+@pytest.mark.parametrize("sym", [T.SYM_SYMMETRIC, T.SYM_SKEW])
+def test_compressed_equals_full(sym):
+    # ref tests/unit/test_engine_split.cpp:272-289
+    levels = [4, 4, 4]
+    g = T.Generator.random(levels, 3, 1.0, sym)
+    v = T.random_vector(levels, 3, 1.0)
+    full = T.Operator.split(g, storage=T.STORAGE_FULL)
+    packed = T.Operator.split(g, storage=T.STORAGE_COMPRESSED)
+    assert packed.kernel_elems < full.kernel_elems
+    yf, mf = full.apply(v, metrics=True)
+    yp, mp = packed.apply(v, metrics=True)
+    assert max_rel(yp, yf) <= 1e-12
+    assert mp["peak_live_elems"] == 4 * 64
+
+
+def test_padding_value_independence():
+    # ref tests/unit/test_engine_split.cpp:140-154
+    levels = [3, 4]
+    g = T.Generator.random(levels, 42, 1.0, T.SYM_GENERAL)
+    v = T.random_vector(levels, 42, 1.0)
+    y0 = T.Operator.split(g).apply(v)
+    for s0 in (1 + 0j, 7 + 3j):
+        assert max_rel(T.Operator.split(g, s0=s0).apply(v), y0) <= 1e-12
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 4])
+def test_counters_and_peak(d):
+    # ref tests/unit/test_engine_split.cpp:156-206
+    levels = [4] * d
+    s = 4 ** d
+    g = T.Generator.random(levels, 23, 1.0, T.SYM_GENERAL)
+    _, m = T.Operator.split(g).apply(T.random_vector(levels, 23, 1.0), metrics=True)
+    assert m["fft_forward"] == 2 ** (d + 1) - 2 == m["fft_inverse"]
+    assert m["diag_mults"] == 2 ** d * s
+    assert m["phase_mults"] == 2 * (2 ** d - 1) * s
+    assert m["peak_live_elems"] == (d + 1) * s
+
+
+def test_parallel_bit_identical_and_deterministic():
+    # ref tests/unit/test_engine_split.cpp:208-252, test_capi.cpp:90-94
+    for d in (2, 3):
+        levels = [4] * d
+        g = T.Generator.random(levels, 11, 1.0, T.SYM_GENERAL)
+        v = T.random_vector(levels, 11, 1.0)
+        op = T.Operator.split(g)
+        lazy = op.apply(v)
+        for budget in (2, 4, 16):
+            par = op.apply(v, policy=(T.POLICY_PARALLEL, budget))
+            assert par.tobytes() == lazy.tobytes()
+        assert op.apply(v).tobytes() == lazy.tobytes()
+
+
+def test_linearity():
+    levels = [4, 3]
+    op = T.Operator.split(T.Generator.random(levels, 31, 1.0, T.SYM_GENERAL))
+    u = T.random_vector(levels, 1, 1.0)
+    v = T.random_vector(levels, 2, 1.0)
+    a, b = 0.7 - 0.3j, -1.2 + 0.4j
+    assert max_rel(op.apply(a * u + b * v), a * op.apply(u) + b * op.apply(v)) <= 1e-12
+
+
+def test_six_levels():
+    # ref tests/unit/test_engine_split.cpp:225-236
+    levels = [2] * 6
+    g = T.Generator.random(levels, 61, 1.0, T.SYM_GENERAL)
+    lags = O.random_lags(levels, 61, 1.0, 0)
+    v = T.random_vector(levels, 61, 1.0)
+    y, m = T.Operator.split(g).apply(v, metrics=True)
+    assert max_rel(y, O.naive(levels, lags, v)) <= 1e-10
+    assert m["fft_forward"] == 2 ** 7 - 2
+    assert m["diag_mults"] == 64 * 64
+    assert m["peak_live_elems"] == 7 * 64
+
+
+def test_kernel_elems_and_tskf_round_trip():
+    # ref tests/capi/test_capi.cpp:64-99,128-162
+    g = T.Generator.random([3, 4], 7, 1.0, T.SYM_SYMMETRIC)
+    op = T.Operator.split(g)
+    assert op.kernel_elems == (3 + 1) * (4 + 1)
+    for sym in (T.SYM_GENERAL, T.SYM_SYMMETRIC):
+        g = T.Generator.random([2, 3], 11, 1.0, sym)
+        op = T.Operator.split(g)
+        v = T.random_vector([2, 3], 11, 1.0)
+        with tempfile.TemporaryDirectory() as td:
+            p = os.path.join(td, "k.tskf")
+            op.save_kernel(p)
+            op2 = T.Operator.load_split(p)
+            assert op.apply(v).tobytes() == op2.apply(v).tobytes()
+    with pytest.raises(T.TsError) as e:
+        T.Operator.load_split("/nonexistent/missing.tskf")
+    assert e.value.code == T.TS_ERR_IO
+
+
+def test_error_codes():
+    lags = np.array([1, 2, 3], np.complex128)
+    g = T.Generator.create([2], lags, T.SYM_GENERAL)
+    with pytest.raises(T.TsError) as e:
+        T.Operator.split(g, storage=T.STORAGE_COMPRESSED)
+    assert e.value.code == T.TS_ERR_SYMMETRY
+    op = T.Operator.split(g)
+    with pytest.raises(T.TsError) as e:
+        op.apply(np.zeros(2, np.complex128), policy=(T.POLICY_LAZY, 0))
+    assert e.value.code == T.TS_ERR_INVALID_ARGUMENT
+
+
+def _dyadic_x(levels, seed):
+    s = int(np.prod(levels))
+    x = O.random_vector([3] + list(levels), seed, 0.5)
+    return [x[i * s:(i + 1) * s] for i in range(3)]
+
+
+@pytest.mark.parametrize("levels", [[6, 6, 6], [8, 8, 8], [5, 6, 7]])
+@pytest.mark.parametrize("prec,tol", [(T.C128, 1e-12), (T.C64, 1e-5)])
+def test_dyadic_3x3_small_vs_reference_composition(levels, prec, tol):
+    # 3x3 composed from 6 scalar reference-style operators, 9 applies
+    # (SURVEY.md §8(c)); the B200 operator stores per-axis-parity compressed
+    # spectra of all 6 unique components.
+    xs = _dyadic_x(levels, 2)
+    ys = O.dyadic_apply(levels, xs, mode="ref")
+    op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec)
+    assert op.info()["storage"] == T.STORAGE_COMPRESSED
+    y = op.apply(np.concatenate(xs))
+    assert rel_l2(y, np.concatenate(ys)) <= tol
+    full = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec,
+                               storage=T.STORAGE_FULL)
+    assert rel_l2(full.apply(np.concatenate(xs)), np.concatenate(ys)) <= tol
+
+
+@pytest.mark.parametrize("nparts", [2, 4, 8])
+def test_partitions_sum_to_full(nparts):
+    levels = [4, 6, 5]
+    for sym in (T.SYM_GENERAL, T.SYM_SYMMETRIC):
+        g = T.Generator.random(levels, 9, 1.0, sym)
+        v = T.random_vector(levels, 9, 1.0)
+        y_full = T.Operator.split(g).apply(v)
+        bg = T.BlockGenerator.from_scalar(g)
+        lags = O.random_lags(levels, 9, 1.0, sym)
+        signs = oracle.axis_signs(3, sym)
+        comp = sym != T.SYM_GENERAL
+        blocks = O.precompute(levels, lags, 0j, comp, signs)
+        acc = np.zeros_like(y_full)
+        for part in range(nparts):
+            op = T.Operator.split_ex(bg, part=part, nparts=nparts)
+            yp = op.apply(v)
+            y_or = O.split_apply_partial(levels, blocks, v, part, nparts, comp, signs)
+            assert rel_l2(yp, y_or) <= 1e-12
+            acc += yp
+        assert rel_l2(acc, y_full) <= 1e-12
+
+
+def test_device_apply_matches_host_apply():
+    import torch
+
+    levels = [8, 8, 8]
+    bg = T.BlockGenerator.dyadic(levels)
+    for prec, dt in ((T.C128, torch.complex128), (T.C64, torch.complex64)):
+        op = T.Operator.split_ex(bg, precision=prec)
+        xs = np.concatenate(_dyadic_x(levels, 3))
+        yh = op.apply(xs)
+        x = torch.from_numpy(xs).to(dt).cuda()
+        y = torch.empty_like(x)
+        m = op.apply_device(x, y, metrics=True)
+        torch.cuda.synchronize()
+        assert rel_l2(y.cpu().numpy().astype(np.complex128), yh) <= (1e-13 if prec == T.C128 else 1e-6)
+        assert m["kernel_elems"] == op.kernel_elems
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("prec,tol", [(T.C128, 1e-12), (T.C64, 1e-5)])
+def test_c1_64cubed_dyadic_vs_oracle(prec, tol):
+    # BASELINE.json configs[1]: 64^3, 3x3 dyadic, x seed 2
+    levels = [64, 64, 64]
+    xs = _dyadic_x(levels, 2)
+    ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+    op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec)
+    y = op.apply(np.concatenate(xs))
+    err = rel_l2(y, ys)
+    assert err <= tol, err
