@@ -107,6 +107,24 @@ typedef struct ts_operator_info {
 
 ts_status ts_operator_get_info(const ts_operator* op, ts_operator_info* out);
 
+/* One kernel launch of an apply, timed with CUDA events on the apply stream. */
+typedef struct ts_launch_record {
+    int32_t kind;          /* 1 = K1 fwd_split, 2 = K2 leaf_pair, 3 = K3 inv_merge,
+                              4 = embed-engine pass */
+    int32_t axis;
+    int32_t single_child;  /* 1 for the partition path variants K1'/K2'/K3' */
+    int32_t reserved;
+    double ms;             /* device time of this launch */
+    uint64_t alg_bytes;    /* algorithmic HBM bytes of this launch (SURVEY.md §8(d)
+                              per-level pass model: vectors + spectra read once) */
+} ts_launch_record;
+
+/* As ts_operator_apply_device, with an event pair around every launch;
+ * synchronizes the stream, then fills out[0..min(cap, launches)) and *count.
+ * For profiling/bench only (events add a few microseconds per launch). */
+ts_status ts_operator_profile_device(const ts_operator* op, const void* x, void* y, void* stream,
+                                     ts_launch_record* out, int32_t cap, int32_t* count);
+
 /* Number of visible CUDA devices (0 when none); never fails. */
 int32_t ts_device_count(void);
 

@@ -42,7 +42,7 @@ EXTENSION_SYMBOLS = [
     "ts_block_generator_create", "ts_block_generator_dyadic", "ts_block_generator_from_scalar",
     "ts_block_generator_components", "ts_block_generator_destroy", "ts_split_options_default",
     "ts_operator_create_split_ex", "ts_operator_apply_device", "ts_operator_get_info",
-    "ts_device_count",
+    "ts_device_count", "ts_operator_profile_device",
 ]
 LAUNCHER_SYMBOLS = [
     "tsk_fwd_split", "tsk_inv_merge", "tsk_leaf_pair", "tsk_embed_generator", "tsk_embed_dyadic",
@@ -89,6 +89,14 @@ class TsOperatorInfo(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class TsLaunchRecord(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("axis", C.c_int32), ("single_child", C.c_int32),
+                ("reserved", C.c_int32), ("ms", C.c_double), ("alg_bytes", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
 _i64p = C.POINTER(C.c_int64)
 _dp = C.POINTER(C.c_double)
 _vp = C.c_void_p
@@ -97,7 +105,7 @@ _vp = C.c_void_p
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is not built; run `python -m paper_2406_17981_b200.build` "
+            f"{LIB_PATH} is not built; run `python paper_2406_17981_b200/build.py` "
             "(there is no CPU fallback)")
     L = C.CDLL(LIB_PATH)
     L.ts_version.restype = C.c_char_p
@@ -136,6 +144,8 @@ def _load():
     L.ts_operator_apply_device.argtypes = [_vp, _vp, _vp, _vp, C.POINTER(TsMetrics)]
     L.ts_operator_get_info.argtypes = [_vp, C.POINTER(TsOperatorInfo)]
     L.ts_device_count.restype = C.c_int32
+    L.ts_operator_profile_device.argtypes = [_vp, _vp, _vp, _vp, C.POINTER(TsLaunchRecord),
+                                             C.c_int32, C.POINTER(C.c_int32)]
     return L
 
 
@@ -223,9 +233,9 @@ class Generator:
         return y
 
     def close(self):
-        if self._h:
+        if self._h and lib is not None:
             lib.ts_generator_destroy(self._h)
-            self._h = None
+        self._h = None
 
     __del__ = close
 
@@ -282,9 +292,9 @@ class BlockGenerator:
         return int(lib.ts_block_generator_components(self._h))
 
     def close(self):
-        if self._h:
+        if self._h and lib is not None:
             lib.ts_block_generator_destroy(self._h)
-            self._h = None
+        self._h = None
 
     __del__ = close
 
@@ -379,9 +389,24 @@ class Operator:
                                          C.c_void_p(stream.cuda_stream), C.byref(m)))
         return m.as_dict() if metrics else None
 
+    def profile_device(self, x, y, stream=None):
+        """Per-launch device times (CUDA events) and algorithmic bytes."""
+        import torch
+
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device)
+        cap = 4096
+        recs = (TsLaunchRecord * cap)()
+        cnt = C.c_int32()
+        _ok(lib.ts_operator_profile_device(self._h, C.c_void_p(x.data_ptr()),
+                                           C.c_void_p(y.data_ptr()),
+                                           C.c_void_p(stream.cuda_stream), recs, cap,
+                                           C.byref(cnt)))
+        return [recs[i].as_dict() for i in range(min(cnt.value, cap))]
+
     def close(self):
-        if self._h:
+        if self._h and lib is not None:
             lib.ts_operator_destroy(self._h)
-            self._h = None
+        self._h = None
 
     __del__ = close

@@ -2,7 +2,7 @@
 a GPU). Objects go to paper_2406_17981_b200/build/, the shared library (plus
 the libtoesplit.so symlink) next to this file so it travels with gpurun.
 
-    python -m paper_2406_17981_b200.build [--force]
+    python paper_2406_17981_b200/build.py [--force]
 """
 from __future__ import annotations
 

@@ -59,7 +59,7 @@ std::vector<cplx> from_interleaved(const double* p, int64_t count)
 {
     need(p != nullptr, "null buffer");
     std::vector<cplx> v(static_cast<size_t>(count));
-    std::memcpy(v.data(), p, static_cast<size_t>(count) * sizeof(cplx));
+    std::memcpy(static_cast<void*>(v.data()), p, static_cast<size_t>(count) * sizeof(cplx));
     return v;
 }
 
@@ -161,8 +161,7 @@ ts_status ts_random_vector(int32_t d, const int64_t* levels, uint64_t seed, doub
 {
     return guarded([&] {
         need(out != nullptr, "null out buffer");
-        auto v = random_vector(check_levels(d, levels), seed, variance);
-        std::memcpy(out, v.data(), v.size() * sizeof(cplx));
+        random_vector_into(check_levels(d, levels), seed, variance, reinterpret_cast<cplx*>(out));
     });
 }
 
@@ -368,6 +367,19 @@ ts_status ts_operator_get_info(const ts_operator* op, ts_operator_info* out)
     return guarded([&] {
         need(op && out);
         operator_info(*op->h.dev, out);
+    });
+}
+
+ts_status ts_operator_profile_device(const ts_operator* op, const void* x, void* y, void* stream,
+                                     ts_launch_record* out, int32_t cap, int32_t* count)
+{
+    return guarded([&] {
+        need(op && count);
+        auto recs = profile_device(*op->h.dev, x, y, stream);
+        const int32_t n = static_cast<int32_t>(recs.size());
+        for (int32_t i = 0; i < n && i < cap && out; ++i)
+            out[i] = recs[i];
+        *count = n;
     });
 }
 

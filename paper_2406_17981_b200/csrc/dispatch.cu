@@ -3,23 +3,54 @@
 // fall back to the generic mixed-radix kernel otherwise.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "tsk_launch.h"
 
 extern "C" int tsk_generic_fwd_split(const tsk_axis* a, void* stream);
 extern "C" int tsk_generic_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_generic_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
+extern "C" int tsk_fast_fwd_split(const tsk_axis* a, void* stream);
+extern "C" int tsk_fast_inv_merge(const tsk_axis* a, void* stream);
+extern "C" int tsk_fast_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
+
+// TSK_GENERIC_ONLY=1 forces the generic kernels (tests cross-check the two).
+static bool generic_only()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TSK_GENERIC_ONLY");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
 
 extern "C" int tsk_fwd_split(const tsk_axis* a, void* stream)
 {
+    if (!generic_only()) {
+        const int e = tsk_fast_fwd_split(a, stream);
+        if (e != -1)
+            return e;
+    }
     return tsk_generic_fwd_split(a, stream);
 }
 
 extern "C" int tsk_inv_merge(const tsk_axis* a, void* stream)
 {
+    if (!generic_only()) {
+        const int e = tsk_fast_inv_merge(a, stream);
+        if (e != -1)
+            return e;
+    }
     return tsk_generic_inv_merge(a, stream);
 }
 
 extern "C" int tsk_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream)
 {
+    if (!generic_only()) {
+        const int e = tsk_fast_leaf_pair(a, sp, stream);
+        if (e != -1)
+            return e;
+    }
     return tsk_generic_leaf_pair(a, sp, stream);
 }

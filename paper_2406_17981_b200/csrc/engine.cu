@@ -97,12 +97,31 @@ struct DevBuf {
     }
 };
 
+// Keep freed stream-ordered memory in the device pool instead of returning it
+// to the driver at every synchronization (the default threshold of 0 would
+// remap the per-call workspace on each apply).
+static void retain_pool()
+{
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev)
+        return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done_dev = dev;
+}
+
 // Stream-ordered scratch (cudaMallocAsync) released on scope exit.
 struct AsyncBuf {
     void* p = nullptr;
     cudaStream_t st = nullptr;
     AsyncBuf(size_t bytes, cudaStream_t s) : st(s)
     {
+        retain_pool();
         if (bytes)
             cuda_check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
     }
@@ -482,8 +501,35 @@ struct Sched {
     cudaStream_t st;
     std::vector<void*> buf;  // child buffer per depth (index 1..d-1)
     int launches = 0;
+    // profiling: an event pair around every launch when rec != nullptr
+    std::vector<ts_launch_record>* rec = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* ev = nullptr;
 
-    int64_t cs() const { return op.s; }
+    uint64_t unit() const { return static_cast<uint64_t>(op.s) * op.m * op.es(); }
+
+    void before()
+    {
+        if (!rec)
+            return;
+        cudaEvent_t a, b;
+        cuda_check(cudaEventCreate(&a), "event");
+        cuda_check(cudaEventCreate(&b), "event");
+        cuda_check(cudaEventRecord(a, st), "event");
+        ev->emplace_back(a, b);
+    }
+    void after(int kind, int axis, int single, uint64_t bytes)
+    {
+        ++launches;
+        if (!rec)
+            return;
+        cuda_check(cudaEventRecord(ev->back().second, st), "event");
+        ts_launch_record r{};
+        r.kind = kind;
+        r.axis = axis;
+        r.single_child = single;
+        r.alg_bytes = bytes;
+        rec->push_back(r);
+    }
 
     tsk_axis ax(int axis) const
     {
@@ -518,8 +564,11 @@ struct Sched {
             sp.skew_mask[u] = op.skew_mask[u];
         for (int i = 0; i < op.m * op.m; ++i)
             sp.comp_map[i] = static_cast<int8_t>(op.comp_map[i]);
+        before();
         launch_check(tsk_leaf_pair(&x, &sp, st), "leaf pair");
-        ++launches;
+        const uint64_t spec = static_cast<uint64_t>(op.n_unique) * op.es() *
+                              ((use_even ? op.block_elems[be] : 0) + (use_odd ? op.block_elems[bo] : 0));
+        after(2, a, !(use_even && use_odd), 2 * unit() + spec);
     }
 
     // Node at depth delta holds data transformed along axes < delta.
@@ -544,8 +593,9 @@ struct Sched {
             f.dst1 = out;
             f.use_even = !odd;
             f.use_odd = odd;
+            before();
             launch_check(tsk_fwd_split(&f, st), "fwd split'");
-            ++launches;
+            after(1, delta, 1, 2 * unit());
             solve(delta + 1, odd ? b | (1u << delta) : b, out, out);
             tsk_axis iv = ax(delta);
             iv.src0 = out;
@@ -554,8 +604,9 @@ struct Sched {
             iv.use_even = !odd;
             iv.use_odd = odd;
             iv.scale = 0.5 / static_cast<double>(op.levels[delta]);
+            before();
             launch_check(tsk_inv_merge(&iv, st), "inv merge'");
-            ++launches;
+            after(3, delta, 1, 2 * unit());
             return;
         }
         void* child = buf[delta + 1];
@@ -563,8 +614,9 @@ struct Sched {
         f.src0 = in;
         f.dst0 = out;
         f.dst1 = child;
+        before();
         launch_check(tsk_fwd_split(&f, st), "fwd split");
-        ++launches;
+        after(1, delta, 0, 3 * unit());
         solve(delta + 1, b, out, out);
         solve(delta + 1, b | (1u << delta), child, child);
         tsk_axis iv = ax(delta);
@@ -572,8 +624,9 @@ struct Sched {
         iv.src1 = child;
         iv.dst0 = out;
         iv.scale = 0.5 / static_cast<double>(op.levels[delta]);
+        before();
         launch_check(tsk_inv_merge(&iv, st), "inv merge");
-        ++launches;
+        after(3, delta, 0, 3 * unit());
     }
 };
 
@@ -615,7 +668,8 @@ void fill_counters(const DeviceOperator& op, ts_metrics* m)
 
 static void apply_embed(const DeviceOperator& op, const void* x, void* y, cudaStream_t st);
 
-static void apply_stream(const DeviceOperator& op, const void* x, void* y, cudaStream_t st)
+static void apply_stream(const DeviceOperator& op, const void* x, void* y, cudaStream_t st,
+                         std::vector<ts_launch_record>* rec = nullptr)
 {
     if (op.is_embed) {
         apply_embed(op, x, y, st);
@@ -624,10 +678,36 @@ static void apply_stream(const DeviceOperator& op, const void* x, void* y, cudaS
     const size_t vbytes = static_cast<size_t>(op.s) * op.m * op.es();
     const int nchild = std::max(0, op.d - 1 - op.q);
     AsyncBuf work(vbytes * nchild, st);
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
     Sched sc{op, st, std::vector<void*>(op.d + 1, nullptr)};
+    sc.rec = rec;
+    sc.ev = &ev;
     for (int i = 0; i < nchild; ++i)
         sc.buf[op.q + 1 + i] = static_cast<char*>(work.p) + vbytes * i;
     sc.solve(0, 0, x, y);
+    if (rec) {
+        cuda_check(cudaStreamSynchronize(st), "profile sync");
+        for (size_t i = 0; i < ev.size(); ++i) {
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, ev[i].first, ev[i].second), "elapsed");
+            (*rec)[i].ms = ms;
+            cudaEventDestroy(ev[i].first);
+            cudaEventDestroy(ev[i].second);
+        }
+    }
+}
+
+std::vector<ts_launch_record> profile_device(const DeviceOperator& op, const void* x, void* y,
+                                             void* stream)
+{
+    if (!x || !y || x == y)
+        fail(TS_ERR_INVALID_ARGUMENT, "x and y must be distinct device buffers");
+    if (op.is_embed)
+        fail(TS_ERR_INVALID_ARGUMENT, "profiling covers split operators");
+    DeviceGuard guard(op.device);
+    std::vector<ts_launch_record> rec;
+    apply_stream(op, x, y, static_cast<cudaStream_t>(stream), &rec);
+    return rec;
 }
 
 void apply_device(const DeviceOperator& op, const void* x, void* y, void* stream,

@@ -75,6 +75,7 @@ struct SplitMix64 {
 SplitMix64 seeded_stream(uint64_t seed, uint64_t role);
 Generator random_generator(const Shape& levels, uint64_t seed, double variance, ts_symmetry sym);
 std::vector<cplx> random_vector(const Shape& levels, uint64_t seed, double variance);
+void random_vector_into(const Shape& levels, uint64_t seed, double variance, cplx* out);
 
 // ---- fixtures and oracle-side host services ---------------------------
 Generator generator_from_json(const std::string& text);
@@ -97,6 +98,8 @@ void apply_host(const DeviceOperator& op, const double* v, double* y, const ts_p
                 ts_metrics* metrics);
 void apply_device(const DeviceOperator& op, const void* x, void* y, void* stream,
                   ts_metrics* metrics);
+std::vector<ts_launch_record> profile_device(const DeviceOperator& op, const void* x, void* y,
+                                             void* stream);
 const Shape& operator_levels(const DeviceOperator& op);
 uint64_t operator_kernel_elems(const DeviceOperator& op);
 void operator_info(const DeviceOperator& op, ts_operator_info* out);

@@ -10,6 +10,7 @@
 #include <fstream>
 #include <numbers>
 #include <sstream>
+#include <thread>
 
 #include "host.hpp"
 
@@ -237,17 +238,50 @@ void symmetrize(std::vector<cplx>& lags, const Shape& levels, bool skew)
 
 }  // namespace
 
+// Complex draws of one stream: element i consumes uniforms 2i and 2i+1 of
+// the SplitMix64 sequence and is exactly one Box-Muller pair (cos part =
+// real, cached sin part = imaginary), so the sequence splits into
+// independent chunks via SplitMix64's additive state (jump = i * gamma).
+// Bit-identical to the sequential GaussianStream of ref instance.cpp.
+static void fill_complex_gaussian(cplx* out, int64_t count, uint64_t seed, uint64_t role,
+                                  double variance)
+{
+    const uint64_t gamma = 0x9E3779B97F4A7C15ull;
+    const uint64_t state0 = seeded_stream(seed, role).state;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int64_t nthreads = count < (int64_t(1) << 16) ? 1 : std::min<int64_t>(hw, 64);
+    auto work = [&](int64_t b, int64_t e) {
+        SplitMix64 rng(state0 + static_cast<uint64_t>(2 * b) * gamma);
+        Gaussian gauss(rng, variance);
+        for (int64_t i = b; i < e; ++i) {
+            const double re = gauss.next();
+            out[i] = cplx{re, gauss.next()};
+        }
+    };
+    if (nthreads == 1) {
+        work(0, count);
+        return;
+    }
+    std::vector<std::thread> th;
+    const int64_t chunk = (count + nthreads - 1) / nthreads;
+    for (int64_t t = 0; t < nthreads; ++t) {
+        const int64_t b = t * chunk, e = std::min(count, b + chunk);
+        if (b < e)
+            th.emplace_back(work, b, e);
+    }
+    for (auto& t : th)
+        t.join();
+}
+
 Generator random_generator(const Shape& levels, uint64_t seed, double variance, ts_symmetry sym)
 {
     int64_t count = 1;
     for (auto n : levels)
         count *= 2 * n - 1;
+    if (!(variance >= 0.0))
+        fail(TS_ERR_INVALID_ARGUMENT, "variance must be >= 0");
     std::vector<cplx> lags(static_cast<size_t>(count));
-    Gaussian gauss(seeded_stream(seed, 0), variance);
-    for (auto& v : lags) {
-        const double re = gauss.next();
-        v = cplx{re, gauss.next()};
-    }
+    fill_complex_gaussian(lags.data(), count, seed, 0, variance);
     if (sym != TS_SYM_GENERAL)
         symmetrize(lags, levels, sym == TS_SYM_SKEW);
     return make_generator(levels, std::move(lags), sym);
@@ -255,13 +289,18 @@ Generator random_generator(const Shape& levels, uint64_t seed, double variance, 
 
 std::vector<cplx> random_vector(const Shape& levels, uint64_t seed, double variance)
 {
+    if (!(variance >= 0.0))
+        fail(TS_ERR_INVALID_ARGUMENT, "variance must be >= 0");
     std::vector<cplx> v(static_cast<size_t>(volume(levels)));
-    Gaussian gauss(seeded_stream(seed, 1), variance);
-    for (auto& x : v) {
-        const double re = gauss.next();
-        x = cplx{re, gauss.next()};
-    }
+    fill_complex_gaussian(v.data(), static_cast<int64_t>(v.size()), seed, 1, variance);
     return v;
+}
+
+void random_vector_into(const Shape& levels, uint64_t seed, double variance, cplx* out)
+{
+    if (!(variance >= 0.0))
+        fail(TS_ERR_INVALID_ARGUMENT, "variance must be >= 0");
+    fill_complex_gaussian(out, volume(levels), seed, 1, variance);
 }
 
 // ---- JSON fixtures (format of ref proj/README.md:144-156) --------------
