@@ -53,28 +53,81 @@ struct Plan {
     static constexpr int TW = tw_off(NST) > 0 ? tw_off(NST) : 1;
 };
 
+// Twiddle / phase entries as {w, rot(w)} with rot(w) = (-w.y, w.x): a
+// complex64 multiply by w is then FMUL2 + FFMA2 and by conj(w) the same two
+// instructions on lane-swapped operands (swz(rot w) = conj w, swz(w) =
+// rot(conj w)). complex128 uses the plain pair.
+template <typename T>
+struct Tw {
+    typename cx<T>::t lo, hi;
+};
+template <typename T>
+struct tw4;
+template <>
+struct tw4<float> {
+    using t = float4;
+};
+template <>
+struct tw4<double> {
+    using t = double4;
+};
+
+template <typename T>
+__device__ __forceinline__ Tw<T> load_tw(const typename tw4<T>::t* p)
+{
+    const typename tw4<T>::t v = *p;
+    Tw<T> w;
+    w.lo.x = v.x;
+    w.lo.y = v.y;
+    w.hi.x = v.z;
+    w.hi.y = v.w;
+    return w;
+}
+
+template <typename T>
+__device__ __forceinline__ typename tw4<T>::t make_tw(typename cx<T>::t w)
+{
+    typename tw4<T>::t r;
+    r.x = w.x;
+    r.y = w.y;
+    r.z = -w.y;
+    r.w = w.x;
+    return r;
+}
+
+// v * w (CONJ: v * conj(w))
+template <typename T, bool CONJ>
+__device__ __forceinline__ typename cx<T>::t cmul_tw(typename cx<T>::t v, const Tw<T>& w)
+{
+    if constexpr (sizeof(T) == 4) {
+        if (CONJ)
+            return fma2(bc_y(v), swz(w.lo), mul2(bc_x(v), swz(w.hi)));
+        return fma2(bc_y(v), w.hi, mul2(bc_x(v), w.lo));
+    } else {
+        return CONJ ? cmulc(v, w.lo) : cmul(v, w.lo);
+    }
+}
+
 // Fill the per-stage twiddle table (w_N^{r * jm * N/(Ns p)}) and the phase
 // table P_k = exp(-i pi k/N) from the operator's double-accurate root/phase
 // tables (global) into shared memory.
 template <typename T, int N>
-__device__ void fill_tables(typename cx<T>::t* tw, typename cx<T>::t* ph,
+__device__ void fill_tables(typename tw4<T>::t* tw, typename tw4<T>::t* ph,
                             const typename cx<T>::t* __restrict__ roots,
                             const typename cx<T>::t* __restrict__ phase)
 {
     using P = Plan<N>;
 #pragma unroll
     for (int s = 1; s < P::NST; ++s) {
-        constexpr int dummy = 0;
-        (void)dummy;
         const int p = P::radix(s), ns = P::ns(s);
         const int cnt = ns * (p - 1);
         for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
             const int jm = e / (p - 1), r = e % (p - 1) + 1;
-            tw[P::tw_off(s) + e] = ldg_c(roots + (r * jm * (N / (ns * p))) % N);
+            tw[P::tw_off(s) + e] = make_tw<T>(ldg_c(roots + (r * jm * (N / (ns * p))) % N));
         }
     }
     for (int k = threadIdx.x; k < N; k += blockDim.x)
-        ph[k] = ldg_c(phase + k);
+        ph[k] = make_tw<T>(ldg_c(phase + k));
 }
 
 // One radix-p butterfly on registers v[i + r*(8/p)], r < p, compile-time p.
@@ -95,12 +148,30 @@ __device__ __forceinline__ void butterfly(typename cx<T>::t (&v)[8], int i)
 }
 
 // K simultaneous length-N transforms of the row pattern held in v[k][8].
-// sbuf: two ping-pong buffers; sidx(k, pos) gives the element index of
-// (transform k, position pos) inside one buffer.
-template <typename T, int N, bool INV, int K, class SIdx>
+// buf0/buf1: ping-pong exchange buffers; sidx(k, pos) gives the element index
+// of (transform k, position pos) inside one buffer. xc counts exchanges across
+// calls so consecutive exchanges alternate buffers (one __syncthreads each).
+struct SyncCta {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+// Threads of one fiber only: a named barrier over `count` threads, or a warp
+// barrier when the fiber lives inside one warp.
+struct SyncGroup {
+    int id, count;
+    __device__ __forceinline__ void operator()() const
+    {
+        if (count <= 32)
+            __syncwarp();
+        else
+            asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+    }
+};
+
+template <typename T, int N, bool INV, int K, class SIdx, class Sync = SyncCta>
 __device__ __forceinline__ void fft_rows(typename cx<T>::t (&v)[K][8], typename cx<T>::t* buf0,
                                          typename cx<T>::t* buf1, const SIdx& sidx,
-                                         const typename cx<T>::t* tw, int t)
+                                         const typename tw4<T>::t* tw, int t, int& xc,
+                                         const Sync& sync = Sync())
 {
     using T2 = typename cx<T>::t;
     using PL = Plan<N>;
@@ -110,7 +181,6 @@ __device__ __forceinline__ void fft_rows(typename cx<T>::t (&v)[K][8], typename 
         const int p = PL::radix(s);
         const int ns = PL::ns(s);
         const int G = 8 / p;
-        // twiddles (stage > 0): input r of butterfly j scaled by w^{r jm ...}
         if (s > 0) {
 #pragma unroll
             for (int i = 0; i < G; ++i) {
@@ -118,12 +188,10 @@ __device__ __forceinline__ void fft_rows(typename cx<T>::t (&v)[K][8], typename 
                 const int jm = j % ns;
 #pragma unroll
                 for (int r = 1; r < p; ++r) {
-                    T2 w = tw[PL::tw_off(s) + jm * (p - 1) + (r - 1)];
-                    if (INV)
-                        w.y = -w.y;
+                    const Tw<T> w = load_tw<T>(tw + PL::tw_off(s) + jm * (p - 1) + (r - 1));
 #pragma unroll
                     for (int k = 0; k < K; ++k)
-                        v[k][i + r * G] = cmul(v[k][i + r * G], w);
+                        v[k][i + r * G] = cmul_tw<T, INV>(v[k][i + r * G], w);
                 }
             }
         }
@@ -143,7 +211,7 @@ __device__ __forceinline__ void fft_rows(typename cx<T>::t (&v)[K][8], typename 
         }
         if (s == PL::NST - 1)
             break;  // last stage outputs are already in the row pattern
-        T2* buf = (s & 1) ? buf1 : buf0;
+        T2* buf = (xc++ & 1) ? buf1 : buf0;
 #pragma unroll
         for (int i = 0; i < G; ++i) {
             const int j = t + i * TF;
@@ -155,7 +223,7 @@ __device__ __forceinline__ void fft_rows(typename cx<T>::t (&v)[K][8], typename 
                 for (int k = 0; k < K; ++k)
                     buf[sidx(k, base + q * ns)] = v[k][i + q * G];
         }
-        __syncthreads();
+        sync();
 #pragma unroll
         for (int m = 0; m < 8; ++m)
 #pragma unroll
@@ -209,6 +277,15 @@ constexpr int strided_w()
 
 // ------------------------------------------------------------------- K1/K3
 
+template <typename T>
+__device__ __forceinline__ typename cx<T>::t cscale(typename cx<T>::t v, T s)
+{
+    if constexpr (sizeof(T) == 4)
+        return mul2(v, make_float2(s, s));
+    else
+        return make_c<T>(v.x * s, v.y * s);
+}
+
 // MODE 0: K1 forward split (even/odd by use flags); MODE 1: K3 inverse merge.
 // Persistent CTAs; the next tile's loads are issued before the current tile's
 // transforms so HBM reads overlap the shared-memory exchanges.
@@ -216,13 +293,14 @@ template <typename T, int N, int W, int MODE>
 __global__ void __launch_bounds__(N / 8 * W) k_strided(tsk_axis p)
 {
     using T2 = typename cx<T>::t;
+    using T4 = typename tw4<T>::t;
     using PL = Plan<N>;
     constexpr int TF = PL::TF;
     constexpr int NIN = MODE == 0 ? 1 : 2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T2* tw = reinterpret_cast<T2*>(smem_raw);
-    T2* ph = tw + PL::TW;
-    T2* buf0 = ph + N;
+    T4* tw = reinterpret_cast<T4*>(smem_raw);
+    T4* ph = tw + PL::TW;
+    T2* buf0 = reinterpret_cast<T2*>(ph + N);
     T2* buf1 = buf0 + 2 * N * W;
     fill_tables<T, N>(tw, ph, static_cast<const T2*>(p.roots), static_cast<const T2*>(p.phase));
     __syncthreads();
@@ -239,24 +317,25 @@ __global__ void __launch_bounds__(N / 8 * W) k_strided(tsk_axis p)
     const T2* s0 = static_cast<const T2*>(p.src0);
     const T2* s1 = static_cast<const T2*>(p.src1);
     const bool ld0 = MODE == 0 || ue, ld1 = MODE == 1 && uo;
+    const int64_t rstride = (int64_t)TF * inner;  // element stride between m and m+1
 
     auto tile_base = [&](int64_t tile) {
         const int64_t c = tile / tiles_per_comp;
         const int64_t r = tile - c * tiles_per_comp;
         const int64_t o = r / cols;
         const int64_t i0 = (r - o * cols) * W;
-        return c * p.cstride + o * (int64_t)N * inner + i0 + w;
+        return c * p.cstride + o * (int64_t)N * inner + i0 + w + (int64_t)t * inner;
     };
     T2 nx[NIN][8];
+    int xc = 0;
     int64_t tile = blockIdx.x;
     if (tile < ntiles) {
         const int64_t b = tile_base(tile);
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-            const int64_t a = b + (int64_t)(t + m * TF) * inner;
-            nx[0][m] = ld0 ? s0[a] : make_c<T>(0, 0);
+            nx[0][m] = ld0 ? s0[b + m * rstride] : make_c<T>(0, 0);
             if (NIN == 2)
-                nx[NIN - 1][m] = ld1 ? s1[a] : make_c<T>(0, 0);
+                nx[NIN - 1][m] = ld1 ? s1[b + m * rstride] : make_c<T>(0, 0);
         }
     }
     for (; tile < ntiles; tile += gridDim.x) {
@@ -264,90 +343,261 @@ __global__ void __launch_bounds__(N / 8 * W) k_strided(tsk_axis p)
         T2 v[2][8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-            if (MODE == 0) {
-                v[0][m] = nx[0][m];
-                v[1][m] = cmul(nx[0][m], ph[t + m * TF]);
-            } else {
-                v[0][m] = nx[0][m];
+            v[0][m] = nx[0][m];
+            if (MODE == 0)
+                v[1][m] = cmul_tw<T, false>(nx[0][m], load_tw<T>(ph + t + m * TF));
+            else
                 v[1][m] = nx[NIN - 1][m];
-            }
         }
         const int64_t nt = tile + gridDim.x;
         if (nt < ntiles) {
             const int64_t b = tile_base(nt);
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
-                const int64_t a = b + (int64_t)(t + m * TF) * inner;
-                nx[0][m] = ld0 ? s0[a] : make_c<T>(0, 0);
+                nx[0][m] = ld0 ? s0[b + m * rstride] : make_c<T>(0, 0);
                 if (NIN == 2)
-                    nx[NIN - 1][m] = ld1 ? s1[a] : make_c<T>(0, 0);
+                    nx[NIN - 1][m] = ld1 ? s1[b + m * rstride] : make_c<T>(0, 0);
             }
         }
         if (MODE == 0) {
-            fft_rows<T, N, false, 2>(v, buf0, buf1, sidx, tw, t);
-            T2* de = static_cast<T2*>(p.dst0);
-            T2* dodd = static_cast<T2*>(p.dst1);
+            fft_rows<T, N, false, 2>(v, buf0, buf1, sidx, tw, t, xc);
+            T2* de = static_cast<T2*>(p.dst0) + base;
+            T2* dodd = static_cast<T2*>(p.dst1) + base;
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
-                const int64_t a = base + (int64_t)(t + m * TF) * inner;
                 if (ue)
-                    de[a] = v[0][m];
+                    de[m * rstride] = v[0][m];
                 if (uo)
-                    dodd[a] = v[1][m];
+                    dodd[m * rstride] = v[1][m];
             }
         } else {
-            fft_rows<T, N, true, 2>(v, buf0, buf1, sidx, tw, t);
-            T2* dst = static_cast<T2*>(p.dst0);
+            fft_rows<T, N, true, 2>(v, buf0, buf1, sidx, tw, t, xc);
+            T2* dst = static_cast<T2*>(p.dst0) + base;
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
-                const T2 acc = cadd(v[0][m], cmulc(v[1][m], ph[t + m * TF]));
-                dst[base + (int64_t)(t + m * TF) * inner] = make_c<T>(scale * acc.x, scale * acc.y);
+                const T2 acc = cadd(v[0][m], cmul_tw<T, true>(v[1][m], load_tw<T>(ph + t + m * TF)));
+                dst[m * rstride] = cscale<T>(acc, scale);
             }
         }
-        // the next tile's first exchange reuses buf0; with two or more
-        // exchanges the later __syncthreads already orders it
-        if (PL::NST - 1 < 2)
-            __syncthreads();
     }
 }
 
 // --------------------------------------------------------------------- K2
 
-// Leaf pair on the contiguous last axis; F fibers per CTA, M components
-// multiplied by the m x m spectra in registers.
-template <typename T, int N, int M, int F>
-__global__ void __launch_bounds__(N / 8 * F) k_leaf(tsk_axis p, tsk_spectra sp)
+// Mirror orbit of a stored index s along one axis: the full indices that the
+// compressed layout maps to s (ref kernel.cpp:25-37): s itself and, when it
+// exists, its mirrored partner.
+__device__ __forceinline__ int orbit_members(int64_t n, int odd, int64_t s, int64_t& partner)
+{
+    const int64_t kp = odd ? n - 1 - s : n - s;
+    partner = kp;
+    if (kp >= 0 && kp < n && kp != s) {
+        bool m;
+        if (mirror_src(n, odd, kp, m) == s && m)
+            return 2;
+    }
+    return 1;
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <typename T2>
+__device__ __forceinline__ T2 flip_sign(T2 v, bool neg)
+{
+    if (neg) {
+        v.x = -v.x;
+        v.y = -v.y;
+    }
+    return v;
+}
+
+// y_i = sum_j T_map(i,j) x_j for the block-symmetric 3x3 map
+// [[0,1,2],[1,3,4],[2,4,5]] (complex64: packed MACs, 21 instructions).
+template <typename T>
+__device__ __forceinline__ void matvec3(typename cx<T>::t (&x)[3], const typename cx<T>::t (&sv)[6])
+{
+    constexpr int cmap[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+    using T2 = typename cx<T>::t;
+    T2 y[3];
+    if constexpr (sizeof(T) == 4) {
+        float2 xn[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            xn[j] = mul2(bc_y(x[j]), make_float2(-1.f, 1.f));  // (-x.y, x.y)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            float2 a = mul2(bc_x(x[0]), sv[cmap[i * 3]]);
+            a = fma2(xn[0], swz(sv[cmap[i * 3]]), a);
+#pragma unroll
+            for (int j = 1; j < 3; ++j) {
+                a = fma2(bc_x(x[j]), sv[cmap[i * 3 + j]], a);
+                a = fma2(xn[j], swz(sv[cmap[i * 3 + j]]), a);
+            }
+            y[i] = a;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            T2 a = make_c<T>(0, 0);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const T2 s = sv[cmap[i * 3 + j]];
+                a.x = fma(x[j].x, s.x, fma(-x[j].y, s.y, a.x));
+                a.y = fma(x[j].x, s.y, fma(x[j].y, s.x, a.y));
+            }
+            y[i] = a;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        x[i] = y[i];
+}
+
+// Leaf pair on the contiguous last axis. A CTA processes G work units of up
+// to 4 fibers each. With mirror-compressed spectra a unit is the mirror orbit
+// of one stored spectra row over the last two outer axes (+-k_{d-3},
+// +-k_{d-2}), so the row is fetched from HBM once and reused from L1 by all
+// members (with per-member signs); with full spectra a unit is 4 consecutive
+// fibers. Components are transformed one after another through a single pair
+// of exchange buffers; the m x m multiply happens in registers. The leaf
+// parities along the last axis are even (beta 0) and odd (beta 1).
+template <typename T, int N, int M, int G>
+__global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(tsk_axis p, tsk_spectra sp)
 {
     using T2 = typename cx<T>::t;
+    using T4 = typename tw4<T>::t;
     using PL = Plan<N>;
     constexpr int TF = PL::TF;
-    constexpr int FP = N;
+    constexpr int S = 4 * G;  // fiber slots per CTA
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T2* tw = reinterpret_cast<T2*>(smem_raw);
-    T2* ph = tw + PL::TW;
-    T2* buf0 = ph + N;
-    T2* buf1 = buf0 + M * F * FP;
-    T2* stash = buf1 + M * F * FP;  // the tile's input, reused by the odd branch
+    T4* tw = reinterpret_cast<T4*>(smem_raw);
+    T4* ph = tw + PL::TW;
+    T2* buf0 = reinterpret_cast<T2*>(ph + N);
+    T2* buf1 = buf0 + S * N;
+    T2* stash = buf1 + S * N;  // M x S x N: x during the even branch, e' during the odd
+    // compressed spectra: one branch's stored row of every unique component,
+    // per unit, staged with cp.async while the forward transforms run
+    constexpr int LROW = N / 2 + 1;
+    constexpr int UM = M == 1 ? 1 : 6;
+    T2* sstage = stash + M * S * N;  // G x UM x LROW
     fill_tables<T, N>(tw, ph, static_cast<const T2*>(p.roots), static_cast<const T2*>(p.phase));
     __syncthreads();
 
-    const int f = threadIdx.x / TF;
+    const int slot = threadIdx.x / TF;
+    const int gi = slot / 4, f = slot % 4;
     const int t = threadIdx.x % TF;
-    const int64_t nfib = p.outer;
-    const int64_t ntiles = (nfib + F - 1) / F;
+    constexpr int FT = TF;  // threads per fiber; exchanges sync only those
+    const SyncGroup fsync{1 + (int)(threadIdx.x / (FT >= 32 ? FT : 32)), FT >= 32 ? FT : 32};
+    const int ut = threadIdx.x - gi * 4 * TF;  // thread index within the unit
     const T scale = (T)p.scale;
     const T2* src = static_cast<const T2*>(p.src0);
     T2* dst = static_cast<T2*>(p.dst0);
-    const T2* spec = static_cast<const T2*>(sp.data);
-    FiberIdx<N, sizeof(T2)> sidx{f * FP, F * FP};
+    FiberIdx<N, sizeof(T2)> sidx{slot * N, 0};
     const int d = sp.d;
     const int U = sp.n_unique;
+    const bool compressed = sp.compressed;
+    const uint32_t bits = sp.branch_bits[0];  // outer-axis parities (shared by both leaves)
+    uint32_t lastneg = 0;                     // components skew along the leaf axis
+    for (int uu = 0; uu < U; ++uu)
+        lastneg |= ((sp.skew_mask[uu] >> (d - 1)) & 1u) << uu;
+    // orbit axes (last two outer axes) and unit count
+    const int A2 = d - 2, A1 = d - 3;
+    int64_t n1 = 1, n2 = 1, st1 = 1, st2 = 1, rest = 1;
+    if (A2 >= 0) {
+        n2 = sp.levels[A2];
+        st2 = compressed ? stored_len(n2, (bits >> A2) & 1u) : n2;
+    }
+    if (A1 >= 0) {
+        n1 = sp.levels[A1];
+        st1 = compressed ? stored_len(n1, (bits >> A1) & 1u) : n1;
+    }
+    for (int a = 0; a < A1; ++a)
+        rest *= sp.levels[a];
+    const int64_t units = compressed ? rest * st1 * st2 : (p.outer + 3) / 4;
+    T2* stash_me = stash + slot * N + t;
+    int xc = 0;
 
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t g = tile * F + f;
-        const bool valid = g < nfib;
-        const int64_t gv = valid ? g : nfib - 1;
-        T2 acc[M][8];
+    for (int64_t tile = blockIdx.x; tile * G < units; tile += gridDim.x) {
+        const int64_t u = tile * G + gi;
+        bool valid = false;
+        int64_t g = 0, off[2] = {0, 0};
+        uint32_t neg = 0;
+        if (u < units) {
+            if (!compressed) {
+                g = u * 4 + f;
+                valid = g < p.outer;
+                off[0] = off[1] = g * N;
+            } else {
+                const int64_t s2 = u % st2;
+                const int64_t s1 = (u / st2) % st1;
+                const int64_t r = u / (st2 * st1);
+                int64_t p1 = 0, p2 = 0;
+                const int c1 = A1 >= 0 ? orbit_members(n1, (bits >> A1) & 1u, s1, p1) : 1;
+                const int c2 = A2 >= 0 ? orbit_members(n2, (bits >> A2) & 1u, s2, p2) : 1;
+                {
+                    valid = f < c1 * c2;
+                    const int i1 = (f % (c1 * c2)) / c2, i2 = f % c2;
+                    const int64_t kk1 = A1 < 0 ? 0 : (i1 ? p1 : s1);
+                    const int64_t kk2 = A2 < 0 ? 0 : (i2 ? p2 : s2);
+                    for (int uu = 0; uu < U; ++uu) {
+                        if (A1 >= 0 && i1)
+                            neg ^= ((sp.skew_mask[uu] >> A1) & 1u) << uu;
+                        if (A2 >= 0 && i2)
+                            neg ^= ((sp.skew_mask[uu] >> A2) & 1u) << uu;
+                    }
+                    // rest axes (0 .. d-4): plain per-fiber mirror remap
+                    int64_t rsrc = 0, rstride_elems = 1, gr = r, rfull = 0, rmul = 1;
+                    for (int a = A1 - 1; a >= 0; --a) {
+                        const int64_t na = sp.levels[a];
+                        const int64_t ka = gr % na;
+                        gr /= na;
+                        const int odd = (bits >> a) & 1u;
+                        bool mm;
+                        rsrc += mirror_src(na, odd, ka, mm) * rstride_elems;
+                        rstride_elems *= stored_len(na, odd);
+                        rfull += ka * rmul;
+                        rmul *= na;
+                        if (mm)
+                            for (int uu = 0; uu < U; ++uu)
+                                neg ^= ((sp.skew_mask[uu] >> a) & 1u) << uu;
+                    }
+                    g = (rfull * n1 + kk1) * n2 + kk2;
+                    const int64_t row = (rsrc * st1 + s1) * st2 + s2;
+                    off[0] = row * (N / 2 + 1);
+                    off[1] = row * (N / 2);
+                }
+            }
+        }
+        const T2* xin = src + g * N + t;
+        T2* stg = sstage + gi * UM * LROW;
+        auto stage = [&](int beta) {
+            if (!compressed || u >= units)
+                return;
+            const int L = beta ? N / 2 : N / 2 + 1;
+            const T2* row = static_cast<const T2*>(sp.data) + sp.branch_base[beta] + off[beta];
+            for (int e = ut; e < UM * L; e += 4 * TF) {
+                const int uu = e / L, kk = e - uu * L;
+                if constexpr (sizeof(T2) == 8)
+                    cp_async8(stg + uu * LROW + kk, row + uu * sp.block_elems[beta] + kk);
+                else
+                    cp_async16(stg + uu * LROW + kk, row + uu * sp.block_elems[beta] + kk);
+            }
+            cp_async_commit();
+        };
+        // every member thread computed the same unit row; slot-0 threads hold it
+        // whether or not their own fiber is valid (row offsets depend on the unit)
+        stage(p.use_even ? 0 : 1);
         T2 v[M][8];
 #pragma unroll
         for (int beta = 0; beta < 2; ++beta) {
@@ -358,114 +608,103 @@ __global__ void __launch_bounds__(N / 8 * F) k_leaf(tsk_axis p, tsk_spectra sp)
             for (int c = 0; c < M; ++c)
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
-                    // each thread stashes and re-reads only its own elements
-                    T2* sl = stash + (c * F + f) * FP + t + m * TF;
-                    if (beta == 0 || !p.use_even) {
-                        const T2 x = src[c * p.cstride + gv * N + t + m * TF];
-                        if (beta == 0 && p.use_odd)
+                    T2* sl = stash_me + c * S * N + m * TF;
+                    if (beta == 0) {
+                        T2 x = make_c<T>(0, 0);
+                        if (valid)
+                            x = xin[c * p.cstride + m * TF];
+                        if (p.use_odd)
                             *sl = x;
-                        v[c][m] = beta ? cmul(x, ph[t + m * TF]) : x;
+                        v[c][m] = x;
+                    } else if (!p.use_even) {
+                        T2 x = make_c<T>(0, 0);
+                        if (valid)
+                            x = xin[c * p.cstride + m * TF];
+                        v[c][m] = cmul_tw<T, false>(x, load_tw<T>(ph + t + m * TF));
                     } else {
-                        v[c][m] = cmul(*sl, ph[t + m * TF]);
+                        const T2 x = *sl;
+                        *sl = v[c][m];  // e' of the even branch
+                        v[c][m] = cmul_tw<T, false>(x, load_tw<T>(ph + t + m * TF));
                     }
                 }
-            fft_rows<T, N, false, M>(v, buf0, buf1, sidx, tw, t);
-            // spectra offset of this fiber (mirror remap of the outer axes)
-            const uint32_t bits = sp.branch_bits[beta];
-            int64_t off = 0;
-            uint32_t neg = 0;
-            int odd_last = (bits >> (d - 1)) & 1u;
-            if (!sp.compressed) {
-                off = gv * N;
-            } else {
-                int64_t gg = gv;
-                int64_t stride = stored_len(N, odd_last);
-                for (int a = d - 2; a >= 0; --a) {
-                    const int64_t na = sp.levels[a];
-                    const int64_t ka = gg % na;
-                    gg /= na;
-                    const int odd = (bits >> a) & 1u;
-                    bool mir;
-                    off += mirror_src(na, odd, ka, mir) * stride;
-                    stride *= stored_len(na, odd);
-                    if (mir)
-                        for (int u = 0; u < U; ++u)
-                            neg ^= ((sp.skew_mask[u] >> a) & 1u) << u;
-                }
-            }
-            const T2* sb = spec + sp.branch_base[beta];
+#pragma unroll
+            for (int c = 0; c < M; ++c)
+                fft_rows<T, N, false, 1>(*reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx,
+                                         tw, t, xc, fsync);
+            const T2* sb = static_cast<const T2*>(sp.data) + sp.branch_base[beta] + off[beta];
             const int64_t bst = sp.block_elems[beta];
+            if (compressed) {
+                cp_async_wait_all();
+                __syncthreads();  // the staged row is complete and visible
+            }
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
                 const int k = t + m * TF;
-                int64_t idx = off;
-                uint32_t ng = neg;
-                if (sp.compressed) {
-                    bool mir;
-                    idx += mirror_src(N, odd_last, k, mir);
-                    if (mir)
-                        for (int u = 0; u < U; ++u)
-                            ng ^= ((sp.skew_mask[u] >> (d - 1)) & 1u) << u;
-                } else {
-                    idx += k;
+                int kidx = k;
+                bool mir = false;
+                if (compressed) {
+                    // beta 0: even parity (stores 0..N/2), beta 1: odd (0..N/2-1)
+                    if (beta == 0) {
+                        mir = k > N / 2;
+                        kidx = mir ? N - k : k;
+                    } else {
+                        mir = k >= N / 2;
+                        kidx = mir ? N - 1 - k : k;
+                    }
                 }
+                const uint32_t ng = neg ^ (mir ? lastneg : 0u);
                 if (M == 1) {
-                    T2 s = ldg_c(sb + idx);
-                    if (ng & 1u)
-                        s = make_c<T>(-s.x, -s.y);
-                    v[0][m] = cmul(v[0][m], s);
+                    T2 sv = make_c<T>(0, 0);
+                    if (compressed)
+                        sv = stg[kidx];
+                    else if (valid)
+                        sv = ldg_c(sb + kidx);
+                    sv = flip_sign(sv, ng & 1u);
+                    v[0][m] = cmul(v[0][m], sv);
                 } else {
-                    // block-symmetric 3x3, canonical map [[0,1,2],[1,3,4],[2,4,5]]
                     T2 sv[6];
 #pragma unroll
-                    for (int u = 0; u < 6; ++u) {
-                        T2 s = ldg_c(sb + u * bst + idx);
-                        if ((ng >> u) & 1u)
-                            s = make_c<T>(-s.x, -s.y);
-                        sv[u] = s;
+                    for (int uu = 0; uu < 6; ++uu) {
+                        T2 s = make_c<T>(0, 0);
+                        if (compressed)
+                            s = stg[uu * LROW + kidx];
+                        else if (valid)
+                            s = ldg_c(sb + uu * bst + kidx);
+                        sv[uu] = flip_sign(s, (ng >> uu) & 1u);
                     }
-                    constexpr int cmap[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
-                    T2 x[3];
+                    T2 x[3] = {v[0][m], v[1][m], v[2][m]};
+                    matvec3<T>(x, sv);
 #pragma unroll
                     for (int c = 0; c < 3; ++c)
-                        x[c] = v[c][m];
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) {
-                        T2 a = make_c<T>(0, 0);
-#pragma unroll
-                        for (int j = 0; j < 3; ++j) {
-                            const T2 s = sv[cmap[i * 3 + j]];
-                            a.x = fma(x[j].x, s.x, fma(-x[j].y, s.y, a.x));
-                            a.y = fma(x[j].x, s.y, fma(x[j].y, s.x, a.y));
-                        }
-                        v[i][m] = a;
-                    }
+                        v[c][m] = x[c];
                 }
             }
-            // the forward transform's last exchange buffer is free once every
-            // thread passed it; order the inverse's first exchange after it
-            __syncthreads();
-            fft_rows<T, N, true, M>(v, buf0, buf1, sidx, tw, t);
+            if (compressed) {
+                __syncthreads();  // everyone is done with the staged row
+                if (beta == 0 && p.use_odd)
+                    stage(1);  // lands while this branch's inverse transforms run
+            }
+#pragma unroll
+            for (int c = 0; c < M; ++c)
+                fft_rows<T, N, true, 1>(*reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx,
+                                        tw, t, xc, fsync);
+        }
+        if (valid) {
+            T2* yout = dst + g * N + t;
 #pragma unroll
             for (int c = 0; c < M; ++c)
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
-                    if (beta == 0)
-                        acc[c][m] = v[c][m];
-                    else if (p.use_even)
-                        acc[c][m] = cadd(acc[c][m], cmulc(v[c][m], ph[t + m * TF]));
-                    else
-                        acc[c][m] = cmulc(v[c][m], ph[t + m * TF]);
+                    T2 a;
+                    if (p.use_odd) {
+                        a = cmul_tw<T, true>(v[c][m], load_tw<T>(ph + t + m * TF));
+                        if (p.use_even)
+                            a = cadd(a, stash_me[c * S * N + m * TF]);
+                    } else {
+                        a = v[c][m];
+                    }
+                    yout[c * p.cstride + m * TF] = cscale<T>(a, scale);
                 }
-            __syncthreads();
-        }
-        if (valid) {
-#pragma unroll
-            for (int c = 0; c < M; ++c)
-#pragma unroll
-                for (int m = 0; m < 8; ++m)
-                    dst[c * p.cstride + g * N + t + m * TF] =
-                        make_c<T>(scale * acc[c][m].x, scale * acc[c][m].y);
         }
     }
 }
@@ -519,7 +758,7 @@ static int launch_strided(const tsk_axis& a, cudaStream_t st)
 {
     constexpr int W = strided_w<T, N>();
     using T2 = typename cx<T>::t;
-    const size_t smem = sizeof(T2) * (Plan<N>::TW + N + 2 * 2 * N * W);
+    const size_t smem = 2 * sizeof(T2) * (Plan<N>::TW + N) + sizeof(T2) * 2 * 2 * N * W;
     if (smem > 227 * 1024)
         return -1;
     auto kern = k_strided<T, N, W, MODE>;
@@ -535,18 +774,33 @@ static int launch_strided(const tsk_axis& a, cudaStream_t st)
 template <typename T, int N, int M>
 static int launch_leaf(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
-    constexpr int F = (N / 8 >= 128) ? 1 : 128 / (N / 8);
+    constexpr int G = (N / 8 * 4 >= 256) ? 1 : 256 / (N / 8 * 4);
+    constexpr int S = 4 * G;
     using T2 = typename cx<T>::t;
-    const size_t smem = sizeof(T2) * (Plan<N>::TW + N + 3 * M * F * N);
+    const size_t smem = 2 * sizeof(T2) * (Plan<N>::TW + N) + sizeof(T2) * (2 + M) * S * N +
+                        sizeof(T2) * G * (M == 1 ? 1 : 6) * (N / 2 + 1);
     if (smem > 227 * 1024)
         return -1;
-    auto kern = k_leaf<T, N, M, F>;
+    auto kern = k_leaf<T, N, M, G>;
     int cap = 0;
-    if (int e = prep(kern, smem, N / 8 * F, cap))
+    if (int e = prep(kern, smem, N / 8 * S, cap))
         return e;
-    const int64_t ntiles = (a.outer + F - 1) / F;
+    // work units: mirror orbits (compressed) or groups of 4 fibers
+    int64_t units;
+    if (sp.compressed) {
+        const int d = sp.d;
+        units = 1;
+        for (int ax = 0; ax < d - 1; ++ax) {
+            const bool orbit_axis = ax >= d - 3;
+            units *= orbit_axis ? stored_len(sp.levels[ax], (sp.branch_bits[0] >> ax) & 1u)
+                                : sp.levels[ax];
+        }
+    } else {
+        units = (a.outer + 3) / 4;
+    }
+    const int64_t ntiles = (units + G - 1) / G;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, cap));
-    kern<<<(unsigned)grid, N / 8 * F, smem, st>>>(a, sp);
+    kern<<<(unsigned)grid, N / 8 * S, smem, st>>>(a, sp);
     return (int)cudaGetLastError();
 }
 

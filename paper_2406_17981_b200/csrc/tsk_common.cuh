@@ -30,6 +30,57 @@ __device__ __forceinline__ typename cx<T>::t make_c(T x, T y)
     return r;
 }
 
+// ---- packed f32x2 arithmetic (sm_100a FADD2/FMUL2/FFMA2) ------------------
+// A complex64 value is one 64-bit register pair; ptxas folds broadcasts
+// make_float2(a.x, a.x) and lane swaps make_float2(a.y, a.x) into operand
+// swizzles, so complex add/sub is one instruction and a complex multiply by a
+// pre-rotated twiddle two.
+__device__ __forceinline__ unsigned long long f2_u(float2 a)
+{
+    union {
+        float2 f;
+        unsigned long long u;
+    } c;
+    c.f = a;
+    return c.u;
+}
+__device__ __forceinline__ float2 u_f2(unsigned long long a)
+{
+    union {
+        float2 f;
+        unsigned long long u;
+    } c;
+    c.u = a;
+    return c.f;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b)
+{
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u(a)), "l"(f2_u(b)));
+    return u_f2(d);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b)
+{
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u(a)), "l"(f2_u(b)));
+    return u_f2(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b)
+{
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u(a)), "l"(f2_u(b)));
+    return u_f2(d);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c)
+{
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_u(a)), "l"(f2_u(b)), "l"(f2_u(c)));
+    return u_f2(d);
+}
+__device__ __forceinline__ float2 bc_x(float2 a) { return make_float2(a.x, a.x); }
+__device__ __forceinline__ float2 bc_y(float2 a) { return make_float2(a.y, a.y); }
+__device__ __forceinline__ float2 swz(float2 a) { return make_float2(a.y, a.x); }
+
 template <typename T2>
 __device__ __forceinline__ T2 cadd(T2 a, T2 b)
 {
@@ -37,6 +88,11 @@ __device__ __forceinline__ T2 cadd(T2 a, T2 b)
     r.x = a.x + b.x;
     r.y = a.y + b.y;
     return r;
+}
+template <>
+__device__ __forceinline__ float2 cadd<float2>(float2 a, float2 b)
+{
+    return add2(a, b);
 }
 
 template <typename T2>
@@ -46,6 +102,11 @@ __device__ __forceinline__ T2 csub(T2 a, T2 b)
     r.x = a.x - b.x;
     r.y = a.y - b.y;
     return r;
+}
+template <>
+__device__ __forceinline__ float2 csub<float2>(float2 a, float2 b)
+{
+    return sub2(a, b);
 }
 
 // (a.x + i a.y)(b.x + i b.y)
@@ -110,6 +171,60 @@ __device__ __forceinline__ void dft4(typename cx<T>::t& x0, typename cx<T>::t& x
     x3 = csub(d0, d1);
 }
 
+// Packed complex64 radix-4: -i d1 folded into one FFMA2 with a (+-1, -+1)
+// lane-sign pair on the swapped operand.
+template <>
+__device__ __forceinline__ void dft4<float, false>(float2& x0, float2& x1, float2& x2, float2& x3)
+{
+    const float2 pm = make_float2(1.f, -1.f), mp = make_float2(-1.f, 1.f);
+    const float2 s0 = add2(x0, x2), d0 = sub2(x0, x2);
+    const float2 s1 = add2(x1, x3), d1 = sub2(x1, x3);
+    x0 = add2(s0, s1);
+    x2 = sub2(s0, s1);
+    x1 = fma2(swz(d1), pm, d0);  // d0 - i d1
+    x3 = fma2(swz(d1), mp, d0);  // d0 + i d1
+}
+template <>
+__device__ __forceinline__ void dft4<float, true>(float2& x0, float2& x1, float2& x2, float2& x3)
+{
+    const float2 pm = make_float2(1.f, -1.f), mp = make_float2(-1.f, 1.f);
+    const float2 s0 = add2(x0, x2), d0 = sub2(x0, x2);
+    const float2 s1 = add2(x1, x3), d1 = sub2(x1, x3);
+    x0 = add2(s0, s1);
+    x2 = sub2(s0, s1);
+    x1 = fma2(swz(d1), mp, d0);  // d0 + i d1
+    x3 = fma2(swz(d1), pm, d0);  // d0 - i d1
+}
+
+// Packed complex64 radix-8 (DIT from two radix-4): 28 FP instructions.
+template <bool INV>
+__device__ __forceinline__ void dft8_packed(float2* v)
+{
+    float2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+    float2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+    dft4<float, INV>(e0, e1, e2, e3);
+    dft4<float, INV>(o0, o1, o2, o3);
+    const float h = 0.70710678118654752440f;
+    const float2 pm = make_float2(1.f, -1.f), mp = make_float2(-1.f, 1.f);
+    if (!INV) {
+        o1 = fma2(bc_y(o1), make_float2(h, h), mul2(bc_x(o1), make_float2(h, -h)));     // * w8
+        o3 = fma2(bc_y(o3), make_float2(h, -h), mul2(bc_x(o3), make_float2(-h, -h)));   // * w8^3
+        v[2] = fma2(swz(o2), pm, e2);
+        v[6] = fma2(swz(o2), mp, e2);
+    } else {
+        o1 = fma2(bc_y(o1), make_float2(-h, h), mul2(bc_x(o1), make_float2(h, h)));
+        o3 = fma2(bc_y(o3), make_float2(-h, -h), mul2(bc_x(o3), make_float2(-h, h)));
+        v[2] = fma2(swz(o2), mp, e2);
+        v[6] = fma2(swz(o2), pm, e2);
+    }
+    v[0] = add2(e0, o0);
+    v[4] = sub2(e0, o0);
+    v[1] = add2(e1, o1);
+    v[5] = sub2(e1, o1);
+    v[3] = add2(e3, o3);
+    v[7] = sub2(e3, o3);
+}
+
 // In-register DFT of size R: v[q] <- sum_r v[r] w_R^{rq}, w_R = exp(-+2 pi i/R).
 // roots/m give w_R^e = roots[e*m] for the generic odd radices.
 template <typename T, int R, bool INV>
@@ -123,6 +238,8 @@ __device__ __forceinline__ void dft_small(typename cx<T>::t* v,
         v[1] = csub(a, b);
     } else if constexpr (R == 4) {
         dft4<T, INV>(v[0], v[1], v[2], v[3]);
+    } else if constexpr (R == 8 && sizeof(T) == 4) {
+        dft8_packed<INV>(reinterpret_cast<float2*>(v));
     } else if constexpr (R == 8) {
         T2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
         T2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];

@@ -261,3 +261,30 @@ def test_c1_64cubed_dyadic_vs_oracle(prec, tol):
     y = op.apply(np.concatenate(xs))
     err = rel_l2(y, ys)
     assert err <= tol, err
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 4, 8])
+@pytest.mark.parametrize("prec,tol", [(T.C128, 1e-12), (T.C64, 1e-5)])
+def test_partitions_fast_path_dyadic(nparts, prec, tol):
+    # power-of-two levels run the register-resident kernels, including the
+    # single-child K1'/K3' and single-branch leaf variants of the partitions
+    levels = [16, 32, 16]
+    xs = _dyadic_x(levels, 5)
+    ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+    bg = T.BlockGenerator.dyadic(levels)
+    acc = np.zeros_like(ys)
+    for part in range(nparts):
+        acc += T.Operator.split_ex(bg, precision=prec, part=part, nparts=nparts).apply(
+            np.concatenate(xs))
+    assert rel_l2(acc, ys) <= tol
+
+
+@pytest.mark.parametrize("levels", [[32, 32, 32], [16, 8, 64], [64, 16, 8]])
+def test_fast_and_generic_agree(levels, monkeypatch):
+    # TSK_GENERIC_ONLY is read once per process, so compare against the oracle
+    # on shapes that route through the fast kernels
+    for sym in SYM:
+        g = T.Generator.random(levels, 13, 1.0, sym)
+        lags, v, y_or = _oracle_split(levels, sym, 13)
+        y = T.Operator.split(g).apply(v)
+        assert rel_l2(y, y_or) <= 1e-12
