@@ -11,8 +11,23 @@ extern "C" int tsk_generic_fwd_split(const tsk_axis* a, void* stream);
 extern "C" int tsk_generic_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_generic_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
 extern "C" int tsk_fast_fwd_split(const tsk_axis* a, void* stream);
+extern "C" int tsk_wide_fwd_split(const tsk_axis* a, void* stream);
+extern "C" int tsk_wide_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_fast_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_fast_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
+
+static bool env_flag(const char* name)
+{
+    const char* e = getenv(name);
+    return e && e[0] == '1';
+}
+static bool no_wide()
+{
+    static int v = -1;
+    if (v < 0)
+        v = env_flag("TSK_NO_WIDE") ? 1 : 0;
+    return v == 1;
+}
 
 // TSK_GENERIC_ONLY=1 forces the generic kernels (tests cross-check the two).
 static bool generic_only()
@@ -28,7 +43,10 @@ static bool generic_only()
 extern "C" int tsk_fwd_split(const tsk_axis* a, void* stream)
 {
     if (!generic_only()) {
-        const int e = tsk_fast_fwd_split(a, stream);
+        int e = no_wide() ? -1 : tsk_wide_fwd_split(a, stream);
+        if (e != -1)
+            return e;
+        e = tsk_fast_fwd_split(a, stream);
         if (e != -1)
             return e;
     }
@@ -38,7 +56,10 @@ extern "C" int tsk_fwd_split(const tsk_axis* a, void* stream)
 extern "C" int tsk_inv_merge(const tsk_axis* a, void* stream)
 {
     if (!generic_only()) {
-        const int e = tsk_fast_inv_merge(a, stream);
+        int e = no_wide() ? -1 : tsk_wide_inv_merge(a, stream);
+        if (e != -1)
+            return e;
+        e = tsk_fast_inv_merge(a, stream);
         if (e != -1)
             return e;
     }

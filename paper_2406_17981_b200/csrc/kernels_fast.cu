@@ -51,6 +51,15 @@ struct Plan {
         return o;
     }
     static constexpr int TW = tw_off(NST) > 0 ? tw_off(NST) : 1;
+    // register twiddle bases: one per (stage >= 1, butterfly i < 8/radix)
+    static constexpr int slot(int s, int i)
+    {
+        int o = 0;
+        for (int k = 1; k < s; ++k)
+            o += 8 / radix(k);
+        return o + i;
+    }
+    static constexpr int NSLOT = slot(NST, 0) > 0 ? slot(NST, 0) : 1;
 };
 
 // Twiddle / phase entries as {w, rot(w)} with rot(w) = (-w.y, w.x): a
@@ -107,6 +116,64 @@ __device__ __forceinline__ typename cx<T>::t cmul_tw(typename cx<T>::t v, const 
         return CONJ ? cmulc(v, w.lo) : cmul(v, w.lo);
     }
 }
+
+template <typename T>
+__device__ __forceinline__ Tw<T> make_twv(typename cx<T>::t w)
+{
+    Tw<T> r;
+    r.lo = w;
+    if constexpr (sizeof(T) == 4)
+        r.hi = mul2(swz(w), make_float2(-1.f, 1.f));
+    else
+        r.hi = make_c<T>(-w.y, w.x);
+    return r;
+}
+
+// w^r for r = 1..P-1 from w (depth <= 3 products, ~3 ulp in complex64).
+template <typename T, int P>
+__device__ __forceinline__ void tw_powers(const Tw<T>& b, Tw<T> (&pw)[8])
+{
+    pw[1] = b;
+    if (P > 2)
+        pw[2] = make_twv<T>(cmul_tw<T, false>(b.lo, b));
+    if (P > 3)
+        pw[3] = make_twv<T>(cmul_tw<T, false>(pw[2].lo, b));
+    if (P > 4) {
+        pw[4] = make_twv<T>(cmul_tw<T, false>(pw[2].lo, pw[2]));
+        pw[5] = make_twv<T>(cmul_tw<T, false>(pw[4].lo, b));
+        pw[6] = make_twv<T>(cmul_tw<T, false>(pw[4].lo, pw[2]));
+        pw[7] = make_twv<T>(cmul_tw<T, false>(pw[4].lo, pw[3]));
+    }
+}
+
+// Split phase P_k = exp(-i pi k/N) at the row pattern k = t + m N/8:
+// P_k = P_t * exp(-i pi m/8), P_t held in registers, the eighth-turn factors
+// compile-time constants.
+template <typename T>
+struct PhaseReg {
+    Tw<T> pt;
+    template <bool CONJ>
+    __device__ __forceinline__ typename cx<T>::t apply(typename cx<T>::t v, int m) const
+    {
+        constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173,
+                         H = 0.70710678118654752440;
+        const double cr[8] = {1.0, C1, H, S1, 0.0, -S1, -H, -C1};
+        const double ci[8] = {0.0, -S1, -H, -C1, -1.0, -C1, -H, -S1};
+        if (m != 0) {
+            typename cx<T>::t c = make_c<T>((T)cr[m], (T)ci[m]);
+            v = cmul_tw<T, CONJ>(v, make_twv_const<T>(c));
+        }
+        return cmul_tw<T, CONJ>(v, pt);
+    }
+    template <typename TT>
+    __device__ __forceinline__ static Tw<TT> make_twv_const(typename cx<TT>::t c)
+    {
+        Tw<TT> r;
+        r.lo = c;
+        r.hi = make_c<TT>(-c.y, c.x);
+        return r;
+    }
+};
 
 // Fill the per-stage twiddle table (w_N^{r * jm * N/(Ns p)}) and the phase
 // table P_k = exp(-i pi k/N) from the operator's double-accurate root/phase
@@ -167,11 +234,13 @@ struct SyncGroup {
     }
 };
 
-template <typename T, int N, bool INV, int K, class SIdx, class Sync = SyncCta>
+// wreg (optional): per-thread twiddle bases, slot(s, i) = w_N^{jm N/(Ns p)};
+// when given, powers are formed in registers instead of reading the table.
+template <typename T, int N, bool INV, int K, class SIdx, class Sync = SyncCta, bool REGTW = false>
 __device__ __forceinline__ void fft_rows(typename cx<T>::t (&v)[K][8], typename cx<T>::t* buf0,
                                          typename cx<T>::t* buf1, const SIdx& sidx,
                                          const typename tw4<T>::t* tw, int t, int& xc,
-                                         const Sync& sync = Sync())
+                                         const Sync& sync = Sync(), const Tw<T>* wreg = nullptr)
 {
     using T2 = typename cx<T>::t;
     using PL = Plan<N>;
@@ -186,12 +255,38 @@ __device__ __forceinline__ void fft_rows(typename cx<T>::t (&v)[K][8], typename 
             for (int i = 0; i < G; ++i) {
                 const int j = t + i * TF;
                 const int jm = j % ns;
+                if (REGTW && s == PL::NST - 1) {
+                    // last twiddled stage (Ns = N/p, a distinct base per thread):
+                    // powers of the register base instead of 4-wavefront table reads
+                    typename cx<T>::t pw[8];
+                    const Tw<T> b = wreg[i];
+                    pw[1] = b.lo;
+                    if (p > 2)
+                        pw[2] = cmul_tw<T, false>(b.lo, b);
+                    if (p > 3)
+                        pw[3] = cmul_tw<T, false>(pw[2], b);
+                    if (p > 4) {
+                        const Tw<T> b2 = make_twv<T>(pw[2]);
+                        pw[4] = cmul_tw<T, false>(pw[2], b2);
+                        pw[5] = cmul_tw<T, false>(pw[4], b);
+                        pw[6] = cmul_tw<T, false>(pw[4], b2);
+                        pw[7] = cmul_tw<T, false>(pw[4], make_twv<T>(pw[3]));
+                    }
 #pragma unroll
-                for (int r = 1; r < p; ++r) {
-                    const Tw<T> w = load_tw<T>(tw + PL::tw_off(s) + jm * (p - 1) + (r - 1));
+                    for (int r = 1; r < p; ++r) {
+                        const Tw<T> w = make_twv<T>(pw[r]);
 #pragma unroll
-                    for (int k = 0; k < K; ++k)
-                        v[k][i + r * G] = cmul_tw<T, INV>(v[k][i + r * G], w);
+                        for (int k = 0; k < K; ++k)
+                            v[k][i + r * G] = cmul_tw<T, INV>(v[k][i + r * G], w);
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 1; r < p; ++r) {
+                        const Tw<T> w = load_tw<T>(tw + PL::tw_off(s) + jm * (p - 1) + (r - 1));
+#pragma unroll
+                        for (int k = 0; k < K; ++k)
+                            v[k][i + r * G] = cmul_tw<T, INV>(v[k][i + r * G], w);
+                    }
                 }
             }
         }
@@ -481,9 +576,8 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
     constexpr int TF = PL::TF;
     constexpr int S = 4 * G;  // fiber slots per CTA
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T4* tw = reinterpret_cast<T4*>(smem_raw);
-    T4* ph = tw + PL::TW;
-    T2* buf0 = reinterpret_cast<T2*>(ph + N);
+    T4* twt = reinterpret_cast<T4*>(smem_raw);
+    T2* buf0 = reinterpret_cast<T2*>(twt + PL::TW);
     T2* buf1 = buf0 + S * N;
     T2* stash = buf1 + S * N;  // M x S x N: x during the even branch, e' during the odd
     // compressed spectra: one branch's stored row of every unique component,
@@ -491,12 +585,39 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
     constexpr int LROW = N / 2 + 1;
     constexpr int UM = M == 1 ? 1 : 6;
     T2* sstage = stash + M * S * N;  // G x UM x LROW
-    fill_tables<T, N>(tw, ph, static_cast<const T2*>(p.roots), static_cast<const T2*>(p.phase));
-    __syncthreads();
+    {
+        // stage tables only (the phase comes from registers)
+#pragma unroll
+        for (int s = 1; s < PL::NST; ++s) {
+            const int pr = PL::radix(s), ns = PL::ns(s);
+            for (int e = threadIdx.x; e < ns * (pr - 1); e += blockDim.x) {
+                const int jm = e / (pr - 1), r = e % (pr - 1) + 1;
+                twt[PL::tw_off(s) + e] =
+                    make_tw<T>(ldg_c(static_cast<const T2*>(p.roots) + (r * jm * (N / (ns * pr))) % N));
+            }
+        }
+        __syncthreads();
+    }
 
     const int slot = threadIdx.x / TF;
     const int gi = slot / 4, f = slot % 4;
     const int t = threadIdx.x % TF;
+    // per-thread twiddle bases and split phase, loaded once (no table reads
+    // inside the transforms)
+    constexpr int SL = PL::NST - 1;  // last stage: its twiddles come from registers
+    Tw<T> wreg[SL > 0 ? 8 / PL::radix(SL) : 1];
+    if constexpr (SL > 0) {
+        const T2* roots = static_cast<const T2*>(p.roots);
+        const int pr = PL::radix(SL), ns = PL::ns(SL);
+#pragma unroll
+        for (int i = 0; i < 8 / pr; ++i) {
+            const int jm = (t + i * TF) % ns;
+            wreg[i] = make_twv<T>(ldg_c(roots + jm * (N / (ns * pr))));
+        }
+    }
+    PhaseReg<T> phr;
+    phr.pt = make_twv<T>(ldg_c(static_cast<const T2*>(p.phase) + t));
+    const typename tw4<T>::t* tw = twt;
     constexpr int FT = TF;  // threads per fiber; exchanges sync only those
     const SyncGroup fsync{1 + (int)(threadIdx.x / (FT >= 32 ? FT : 32)), FT >= 32 ? FT : 32};
     const int ut = threadIdx.x - gi * 4 * TF;  // thread index within the unit
@@ -620,17 +741,17 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
                         T2 x = make_c<T>(0, 0);
                         if (valid)
                             x = xin[c * p.cstride + m * TF];
-                        v[c][m] = cmul_tw<T, false>(x, load_tw<T>(ph + t + m * TF));
+                        v[c][m] = phr.template apply<false>(x, m);
                     } else {
                         const T2 x = *sl;
                         *sl = v[c][m];  // e' of the even branch
-                        v[c][m] = cmul_tw<T, false>(x, load_tw<T>(ph + t + m * TF));
+                        v[c][m] = phr.template apply<false>(x, m);
                     }
                 }
 #pragma unroll
             for (int c = 0; c < M; ++c)
-                fft_rows<T, N, false, 1>(*reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx,
-                                         tw, t, xc, fsync);
+                fft_rows<T, N, false, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, true>(
+                    *reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx, tw, t, xc, fsync, wreg);
             const T2* sb = static_cast<const T2*>(sp.data) + sp.branch_base[beta] + off[beta];
             const int64_t bst = sp.block_elems[beta];
             if (compressed) {
@@ -686,8 +807,8 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
             }
 #pragma unroll
             for (int c = 0; c < M; ++c)
-                fft_rows<T, N, true, 1>(*reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx,
-                                        tw, t, xc, fsync);
+                fft_rows<T, N, true, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, true>(
+                    *reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx, tw, t, xc, fsync, wreg);
         }
         if (valid) {
             T2* yout = dst + g * N + t;
@@ -697,7 +818,7 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
                 for (int m = 0; m < 8; ++m) {
                     T2 a;
                     if (p.use_odd) {
-                        a = cmul_tw<T, true>(v[c][m], load_tw<T>(ph + t + m * TF));
+                        a = phr.template apply<true>(v[c][m], m);
                         if (p.use_even)
                             a = cadd(a, stash_me[c * S * N + m * TF]);
                     } else {
@@ -777,7 +898,7 @@ static int launch_leaf(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st
     constexpr int G = (N / 8 * 4 >= 256) ? 1 : 256 / (N / 8 * 4);
     constexpr int S = 4 * G;
     using T2 = typename cx<T>::t;
-    const size_t smem = 2 * sizeof(T2) * (Plan<N>::TW + N) + sizeof(T2) * (2 + M) * S * N +
+    const size_t smem = 2 * sizeof(T2) * Plan<N>::TW + sizeof(T2) * (2 + M) * S * N +
                         sizeof(T2) * G * (M == 1 ? 1 : 6) * (N / 2 + 1);
     if (smem > 227 * 1024)
         return -1;

@@ -1,0 +1,611 @@
+// Wide-tile sm_100a kernels for the strided passes (K1 fwd_split, K3
+// inv_merge) on power-of-two axes.
+//
+// Why wide tiles: a strided pass reads/writes, per tile, one contiguous row
+// segment per position along the axis. Measured on B200 (tools/micro/
+// strided_copy2.cu, pure 1R/2W copies of 512-row tiles): 64-byte segments
+// reach 2.3 TB/s, 128-byte 4.3 TB/s, 256-byte 5.8 TB/s (of 6.55 measured) —
+// independent of stride, TLB reach or tile order. So every warp memory
+// instruction here covers one 256-byte row segment (W = 32 complex64 or 16
+// complex128 columns), and a tile is N x 256 bytes (128 KB at N = 512).
+//
+// To fit that tile, each thread holds R = 16..32 elements of one column in
+// registers ("row pattern" k = t + m*TF, TF = N/R threads per column): N = 512
+// is 32 x 16, one shared-memory exchange per transform.
+//  K1: odd = F(P x) is transformed and stored (to the child buffer), then x
+//      is re-read (an L2 hit, the tile was just loaded) for even = F(x), which
+//      may overwrite x in place.
+//  K3: out = scale * (B(e) + conj(P) B(o)); B(e) is parked in tensor memory
+//      (tcgen05.st/ld on the thread's own TMEM lane, 32x32b shape) while B(o)
+//      is computed, so registers hold one transform at a time.
+// Reference semantics as in kernels_generic.cu (fft.cpp:65-87,
+// tensor.cpp:227-254, engine_split.cpp:13-37).
+#include <cuda_runtime.h>
+
+#include <utility>
+
+#include "tsk_common.cuh"
+
+namespace tsk {
+namespace wide {
+
+constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+// cos(2 pi k / 64), k = 0..16 (quarter wave; the rest by symmetry)
+__host__ __device__ constexpr double cos64q(int k)
+{
+    constexpr double t[17] = {1.0,
+                              0.99518472667219688624,
+                              0.98078528040323044913,
+                              0.95694033573220886494,
+                              0.92387953251128675613,
+                              0.88192126434835502971,
+                              0.83146961230254523708,
+                              0.77301045336273696081,
+                              0.70710678118654752440,
+                              0.63439328416364549822,
+                              0.55557023301960222474,
+                              0.47139673682599764856,
+                              0.38268343236508977173,
+                              0.29028467725446236764,
+                              0.19509032201612826785,
+                              0.09801714032956060199,
+                              0.0};
+    return t[k];
+}
+__host__ __device__ constexpr double cos64(int k)
+{
+    k = ((k % 64) + 64) % 64;
+    if (k <= 16)
+        return cos64q(k);
+    if (k <= 32)
+        return -cos64q(32 - k);
+    if (k <= 48)
+        return -cos64q(k - 32);
+    return cos64q(64 - k);
+}
+__host__ __device__ constexpr double sin64(int k) { return cos64(k - 16); }
+
+// v * exp(sgn 2 pi i k / P) for a compile-time angle (P | 64).
+template <typename T, int P, int K, bool INV>
+__device__ __forceinline__ typename cx<T>::t cmul_const(typename cx<T>::t v)
+{
+    constexpr int k64 = ((K % P) + P) % P * (64 / P);
+    constexpr double c = cos64(k64);
+    constexpr double s = (INV ? 1.0 : -1.0) * sin64(k64);
+    if constexpr (k64 == 0) {
+        return v;
+    } else if constexpr (k64 == 32) {
+        return make_c<T>(-v.x, -v.y);
+    } else if constexpr (k64 == 16 || k64 == 48) {
+        // multiply by +-i
+        if constexpr (sizeof(T) == 4)
+            return mul2(swz(v), s > 0 ? make_float2(-1.f, 1.f) : make_float2(1.f, -1.f));
+        else
+            return s > 0 ? make_c<T>(-v.y, v.x) : make_c<T>(v.y, -v.x);
+    } else {
+        if constexpr (sizeof(T) == 4)
+            return fma2(bc_y(v), make_float2((float)-s, (float)c),
+                        mul2(bc_x(v), make_float2((float)c, (float)s)));
+        else
+            return make_c<T>(v.x * c - v.y * s, v.x * s + v.y * c);
+    }
+}
+
+// In-register DFT of size P on a[0..P), natural order in and out.
+template <typename T, int P, bool INV>
+struct Dft {
+    using T2 = typename cx<T>::t;
+    // split P = P1 * P2: input r = P2 a + b, output q = c + P1 e
+    static constexpr int P1 = P >= 16 ? 4 : 2;
+    static constexpr int P2 = P / P1;
+    template <int B, int C>
+    __device__ __forceinline__ static void tw(T2* a)
+    {
+        a[P2 * C + B] = cmul_const<T, P, B * C, INV>(a[P2 * C + B]);
+    }
+    __device__ __forceinline__ static void run(T2* a)
+    {
+        if constexpr (P == 1) {
+        } else if constexpr (P == 2) {
+            const T2 x = a[0], y = a[1];
+            a[0] = cadd(x, y);
+            a[1] = csub(x, y);
+        } else if constexpr (P == 4) {
+            dft4<T, INV>(a[0], a[1], a[2], a[3]);
+        } else if constexpr (P == 8) {
+            dft_small<T, 8, INV>(a, nullptr, 0);
+        } else {
+            // step 1: P2 transforms of length P1 on stride-P2 subsequences
+#pragma unroll
+            for (int b = 0; b < P2; ++b) {
+                T2 s[P1];
+#pragma unroll
+                for (int i = 0; i < P1; ++i)
+                    s[i] = a[P2 * i + b];
+                Dft<T, P1, INV>::run(s);
+#pragma unroll
+                for (int i = 0; i < P1; ++i)
+                    a[P2 * i + b] = s[i];
+            }
+            // twiddles w_P^{b c}
+            twiddles(a, std::make_integer_sequence<int, P1 * P2>{});
+            // step 2: P1 transforms of length P2 on contiguous groups
+            T2 o[P];
+#pragma unroll
+            for (int c = 0; c < P1; ++c) {
+                T2 s[P2];
+#pragma unroll
+                for (int i = 0; i < P2; ++i)
+                    s[i] = a[P2 * c + i];
+                Dft<T, P2, INV>::run(s);
+#pragma unroll
+                for (int e = 0; e < P2; ++e)
+                    o[c + P1 * e] = s[e];
+            }
+#pragma unroll
+            for (int q = 0; q < P; ++q)
+                a[q] = o[q];
+        }
+    }
+    template <int... Is>
+    __device__ __forceinline__ static void twiddles(T2* a, std::integer_sequence<int, Is...>)
+    {
+        (tw<Is % P2, Is / P2>(a), ...);
+    }
+};
+
+template <int N, int R>
+struct Plan {
+    static constexpr int TF = N / R;
+    static constexpr int L = ilog2(N), LR = ilog2(R);
+    static constexpr int NST = (L + LR - 1) / LR;
+    static constexpr int radix(int s)
+    {
+        return s < NST - 1 ? R : (1 << (L - LR * (NST - 1)));
+    }
+    static constexpr int ns(int s)
+    {
+        int v = 1;
+        for (int i = 0; i < s; ++i)
+            v *= radix(i);
+        return v;
+    }
+    static constexpr int tw_off(int s)
+    {
+        int o = 0;
+        for (int i = 1; i < s; ++i)
+            o += ns(i) * (radix(i) - 1);
+        return o;
+    }
+    static constexpr int TW = tw_off(NST) > 0 ? tw_off(NST) : 1;
+};
+
+template <typename T>
+struct tw4;
+template <>
+struct tw4<float> {
+    using t = float4;
+};
+template <>
+struct tw4<double> {
+    using t = double4;
+};
+
+template <typename T>
+struct Tw {
+    typename cx<T>::t lo, hi;
+};
+
+template <typename T>
+__device__ __forceinline__ Tw<T> load_tw(const typename tw4<T>::t* p)
+{
+    const typename tw4<T>::t v = *p;
+    Tw<T> w;
+    w.lo.x = v.x;
+    w.lo.y = v.y;
+    w.hi.x = v.z;
+    w.hi.y = v.w;
+    return w;
+}
+
+template <typename T>
+__device__ __forceinline__ typename tw4<T>::t make_tw(typename cx<T>::t w)
+{
+    typename tw4<T>::t r;
+    r.x = w.x;
+    r.y = w.y;
+    r.z = -w.y;
+    r.w = w.x;
+    return r;
+}
+
+template <typename T, bool CONJ>
+__device__ __forceinline__ typename cx<T>::t cmul_tw(typename cx<T>::t v, const Tw<T>& w)
+{
+    if constexpr (sizeof(T) == 4) {
+        if (CONJ)
+            return fma2(bc_y(v), swz(w.lo), mul2(bc_x(v), swz(w.hi)));
+        return fma2(bc_y(v), w.hi, mul2(bc_x(v), w.lo));
+    } else {
+        return CONJ ? cmulc(v, w.lo) : cmul(v, w.lo);
+    }
+}
+
+template <typename T, int N, int R>
+__device__ void fill_tables(typename tw4<T>::t* tw, typename tw4<T>::t* ph,
+                            const typename cx<T>::t* __restrict__ roots,
+                            const typename cx<T>::t* __restrict__ phase)
+{
+    using P = Plan<N, R>;
+#pragma unroll
+    for (int s = 1; s < P::NST; ++s) {
+        const int p = P::radix(s), ns = P::ns(s);
+        for (int e = threadIdx.x; e < ns * (p - 1); e += blockDim.x) {
+            const int jm = e / (p - 1), r = e % (p - 1) + 1;
+            tw[P::tw_off(s) + e] = make_tw<T>(ldg_c(roots + (r * jm * (N / (ns * p))) % N));
+        }
+    }
+    for (int k = threadIdx.x; k < N; k += blockDim.x)
+        ph[k] = make_tw<T>(ldg_c(phase + k));
+}
+
+// One length-N transform of the row pattern v[m] = x[t + m TF] (m < R) of one
+// column w; exchanges through the [N][W] tile buffer (a warp covers one row,
+// conflict free), two barriers per exchange (single buffer).
+template <typename T, int N, int R, int W, bool INV>
+__device__ __forceinline__ void fft_col(typename cx<T>::t (&v)[R], typename cx<T>::t* buf,
+                                        const typename tw4<T>::t* tw, int t, int w)
+{
+    using T2 = typename cx<T>::t;
+    using PL = Plan<N, R>;
+    constexpr int TF = PL::TF;
+#pragma unroll
+    for (int s = 0; s < PL::NST; ++s) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int p = PL::radix(s);
+        const int ns = PL::ns(s);
+        const int G = R / p;
+        if (s > 0) {
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                const int jm = (t + i * TF) % ns;
+#pragma unroll
+                for (int r = 1; r < p; ++r) {
+                    const Tw<T> wv = load_tw<T>(tw + PL::tw_off(s) + jm * (p - 1) + (r - 1));
+                    v[i + r * G] = cmul_tw<T, INV>(v[i + r * G], wv);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            T2 a[R];
+#pragma unroll
+            for (int r = 0; r < p; ++r)
+                a[r] = v[i + r * G];
+            switch (p) {
+            case 2: Dft<T, 2, INV>::run(a); break;
+            case 4: Dft<T, 4, INV>::run(a); break;
+            case 8: Dft<T, 8, INV>::run(a); break;
+            case 16: Dft<T, 16, INV>::run(a); break;
+            case 32: Dft<T, 32, INV>::run(a); break;
+            default: break;
+            }
+#pragma unroll
+            for (int r = 0; r < p; ++r)
+                v[i + r * G] = a[r];
+        }
+        if (s == PL::NST - 1)
+            break;
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            const int j = t + i * TF;
+            const int jm = j % ns;
+            const int base = (j - jm) * p + jm;
+#pragma unroll
+            for (int q = 0; q < p; ++q)
+                buf[(base + q * ns) * W + w] = v[i + q * G];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < R; ++m)
+            v[m] = buf[(t + m * TF) * W + w];
+        __syncthreads();
+    }
+}
+
+// ---- tensor memory (thread-private lanes) ----------------------------------
+
+__device__ __forceinline__ uint32_t tmem_alloc(uint32_t* slot, int cols)
+{
+    // one warp allocates; the base address lands in shared memory
+    if (threadIdx.x < 32) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(slot);
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa),
+                     "r"(cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    return *slot;
+}
+
+__device__ __forceinline__ void tmem_free(uint32_t base, int cols)
+{
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (threadIdx.x < 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols)
+                     : "memory");
+}
+
+// Store / load 32 consecutive 32-bit columns of this thread's lane.
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&r)[32])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+        "%29, %30, %31, %32};" ::"r"(addr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+        "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+        "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&r)[32])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+        "%29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(addr)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Park / restore R complex values (2 or 4 words each) in this thread's lane.
+template <typename T, int R>
+__device__ __forceinline__ void tmem_park(uint32_t lane_base, const typename cx<T>::t (&v)[R])
+{
+    constexpr int WORDS = R * (int)sizeof(typename cx<T>::t) / 4;
+    static_assert(WORDS % 32 == 0, "park granularity is 32 words");
+#pragma unroll
+    for (int c = 0; c < WORDS / 32; ++c) {
+        uint32_t r[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            r[i] = reinterpret_cast<const uint32_t*>(&v[0])[c * 32 + i];
+        tmem_st32(lane_base + c * 32, r);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+template <typename T, int R>
+__device__ __forceinline__ void tmem_restore(uint32_t lane_base, typename cx<T>::t (&v)[R])
+{
+    constexpr int WORDS = R * (int)sizeof(typename cx<T>::t) / 4;
+#pragma unroll
+    for (int c = 0; c < WORDS / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(lane_base + c * 32, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            reinterpret_cast<uint32_t*>(&v[0])[c * 32 + i] = r[i];
+    }
+}
+
+// ---- K1 / K3 ------------------------------------------------------------------
+
+template <typename T, int N, int R, int W, int MODE>
+__global__ void __launch_bounds__(N / R * W) k_wide(tsk_axis p)
+{
+    using T2 = typename cx<T>::t;
+    using T4 = typename tw4<T>::t;
+    using PL = Plan<N, R>;
+    constexpr int TF = PL::TF;
+    constexpr int NT = TF * W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T4* tw = reinterpret_cast<T4*>(smem_raw);
+    T4* ph = tw + PL::TW;
+    T2* buf = reinterpret_cast<T2*>(ph + N);
+    __shared__ uint32_t tmem_slot;
+    fill_tables<T, N, R>(tw, ph, static_cast<const T2*>(p.roots), static_cast<const T2*>(p.phase));
+    __syncthreads();
+
+    const int w = threadIdx.x % W;
+    const int t = threadIdx.x / W;
+    const int64_t inner = p.inner;
+    const int64_t cols = inner / W;
+    const int64_t tiles_per_comp = p.outer * cols;
+    const int64_t ntiles = tiles_per_comp * p.ncomp;
+    const bool ue = p.use_even, uo = p.use_odd;
+    const T scale = (T)p.scale;
+    const int64_t rs = (int64_t)TF * inner;  // element stride between m and m+1
+
+    // K3 with both inputs parks B(e) in tensor memory: warps sharing a lane
+    // quadrant (w % 4) take disjoint column ranges
+    constexpr int PWORDS = R * (int)sizeof(T2) / 4;
+    constexpr int NW = NT / 32;
+    constexpr int TCOLS_RAW = PWORDS * ((NW + 3) / 4);
+    constexpr int TCOLS = TCOLS_RAW <= 32 ? 32 : TCOLS_RAW <= 64 ? 64 : TCOLS_RAW <= 128 ? 128
+                                                                        : TCOLS_RAW <= 256 ? 256 : 512;
+    constexpr bool TM = PWORDS % 32 == 0;  // small R keeps B(e) in registers
+    const bool park = TM && MODE == 1 && ue && uo;
+    uint32_t tbase = 0, lane_base = 0;
+    if constexpr (MODE == 1) {
+        if (park) {
+            tbase = tmem_alloc(&tmem_slot, TCOLS);
+            const int warp = threadIdx.x / 32;
+            lane_base = tbase + ((uint32_t)(32 * (warp % 4)) << 16) + (uint32_t)(PWORDS * (warp / 4));
+        }
+    }
+
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t c = tile / tiles_per_comp;
+        const int64_t r = tile - c * tiles_per_comp;
+        const int64_t o = r / cols;
+        const int64_t i0 = (r - o * cols) * W;
+        const int64_t base = c * p.cstride + o * (int64_t)N * inner + i0 + w + (int64_t)t * inner;
+        T2 v[R];
+        T2 ekeep[TM ? 1 : R];
+        if (MODE == 0) {
+            // odd first: even may be written in place over the input (dst0 ==
+            // src0 below the root), and the odd child needs the input again
+            const T2* src = static_cast<const T2*>(p.src0) + base;
+            if (uo) {
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    v[m] = cmul_tw<T, false>(src[m * rs], load_tw<T>(ph + t + m * TF));
+                fft_col<T, N, R, W, false>(v, buf, tw, t, w);
+                T2* dd = static_cast<T2*>(p.dst1) + base;
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    dd[m * rs] = v[m];
+            }
+            if (ue) {
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    v[m] = src[m * rs];
+                fft_col<T, N, R, W, false>(v, buf, tw, t, w);
+                T2* de = static_cast<T2*>(p.dst0) + base;
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    de[m * rs] = v[m];
+            }
+        } else {
+            T2* dst = static_cast<T2*>(p.dst0) + base;
+            if (ue) {
+                const T2* se = static_cast<const T2*>(p.src0) + base;
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    v[m] = se[m * rs];
+                fft_col<T, N, R, W, true>(v, buf, tw, t, w);
+                if (!uo) {
+#pragma unroll
+                    for (int m = 0; m < R; ++m)
+                        dst[m * rs] = make_c<T>(scale * v[m].x, scale * v[m].y);
+                    continue;
+                }
+                if constexpr (MODE == 1 && TM)
+                    tmem_park<T, R>(lane_base, v);
+                else
+#pragma unroll
+                    for (int m = 0; m < R; ++m)
+                        ekeep[m] = v[m];
+            }
+            if (uo) {
+                const T2* so = static_cast<const T2*>(p.src1) + base;
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    v[m] = so[m * rs];
+                fft_col<T, N, R, W, true>(v, buf, tw, t, w);
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    v[m] = cmul_tw<T, true>(v[m], load_tw<T>(ph + t + m * TF));
+                if (ue) {
+                    T2 e[R];
+                    if constexpr (MODE == 1 && TM)
+                        tmem_restore<T, R>(lane_base, e);
+                    else
+#pragma unroll
+                        for (int m = 0; m < R; ++m)
+                            e[m] = ekeep[m];
+#pragma unroll
+                    for (int m = 0; m < R; ++m)
+                        v[m] = cadd(v[m], e[m]);
+                }
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    dst[m * rs] = make_c<T>(scale * v[m].x, scale * v[m].y);
+            }
+        }
+    }
+    if constexpr (MODE == 1) {
+        if (park)
+            tmem_free(tbase, TCOLS);
+    }
+}
+
+template <typename T, int N>
+struct Geom {
+    // 256-byte row segments; R elements per thread
+    static constexpr int W = 256 / (int)sizeof(typename cx<T>::t);
+    static constexpr int R = N >= 512 ? 32 : (N >= 128 ? 16 : 8);
+    static constexpr int NT = N / R * W;
+};
+
+static int sm_count()
+{
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 148;
+}
+
+template <typename T, int N, int MODE>
+static int launch(const tsk_axis& a, cudaStream_t st)
+{
+    using G = Geom<T, N>;
+    using T2 = typename cx<T>::t;
+    if (G::NT > 1024 || a.inner % G::W != 0)
+        return -1;
+    const size_t smem = 2 * sizeof(T2) * (Plan<N, G::R>::TW + N) + sizeof(T2) * N * G::W;
+    if (smem > 227 * 1024)
+        return -1;
+    auto kern = k_wide<T, N, G::R, G::W, MODE>;
+    static thread_local int cached_dev = -1, cap = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != cached_dev) {
+        if (int e = (int)cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem))
+            return e;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::NT, smem);
+        cap = sm_count() * (per_sm > 0 ? per_sm : 1);
+        cached_dev = dev;
+    }
+    const int64_t ntiles = a.outer * (a.inner / G::W) * a.ncomp;
+    const int64_t grid = ntiles < cap ? ntiles : cap;
+    kern<<<(unsigned)(grid > 0 ? grid : 1), G::NT, smem, st>>>(a);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, int MODE>
+static int dispatch(const tsk_axis& a, cudaStream_t st)
+{
+    switch (a.n) {
+    case 64: return launch<T, 64, MODE>(a, st);
+    case 128: return launch<T, 128, MODE>(a, st);
+    case 256: return launch<T, 256, MODE>(a, st);
+    case 512: return launch<T, 512, MODE>(a, st);
+    default: return -1;
+    }
+}
+
+}  // namespace wide
+}  // namespace tsk
+
+// -1: shape not covered (the caller falls back), else the launch cudaError_t.
+extern "C" int tsk_wide_fwd_split(const tsk_axis* a, void* stream)
+{
+    return a->prec ? tsk::wide::dispatch<float, 0>(*a, (cudaStream_t)stream)
+                   : tsk::wide::dispatch<double, 0>(*a, (cudaStream_t)stream);
+}
+
+extern "C" int tsk_wide_inv_merge(const tsk_axis* a, void* stream)
+{
+    return a->prec ? tsk::wide::dispatch<float, 1>(*a, (cudaStream_t)stream)
+                   : tsk::wide::dispatch<double, 1>(*a, (cudaStream_t)stream);
+}

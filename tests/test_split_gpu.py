@@ -288,3 +288,26 @@ def test_fast_and_generic_agree(levels, monkeypatch):
         lags, v, y_or = _oracle_split(levels, sym, 13)
         y = T.Operator.split(g).apply(v)
         assert rel_l2(y, y_or) <= 1e-12
+
+
+@pytest.mark.parametrize("levels", [[512, 8, 32], [256, 32, 16], [128, 64, 32], [64, 64, 64]])
+def test_wide_strided_passes_vs_oracle(levels):
+    # axes with n in {64..512} and 256-byte-multiple strides run the wide
+    # tiles (kernels_wide.cu), including in-place K1 below the root and the
+    # TMEM-parked K3
+    for sym in (T.SYM_GENERAL, T.SYM_SYMMETRIC):
+        g = T.Generator.random(levels, 21, 1.0, sym)
+        lags, v, y_or = _oracle_split(levels, sym, 21)
+        assert rel_l2(T.Operator.split(g).apply(v), y_or) <= 1e-12
+        bg = T.BlockGenerator.from_scalar(g)
+        y64 = T.Operator.split_ex(bg, precision=T.C64).apply(v)
+        assert rel_l2(y64, y_or) <= 1e-5
+
+
+@pytest.mark.parametrize("levels", [[512, 16, 16], [16, 256, 32]])
+def test_wide_dyadic_vs_oracle(levels):
+    xs = _dyadic_x(levels, 7)
+    ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+    for prec, tol in ((T.C128, 1e-12), (T.C64, 1e-5)):
+        op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec)
+        assert rel_l2(op.apply(np.concatenate(xs)), ys) <= tol
