@@ -19,6 +19,8 @@
 // tensor.cpp:227-254, engine_split.cpp:13-37, kernel.cpp:126-219).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "tsk_common.cuh"
 
 namespace tsk {
@@ -81,15 +83,17 @@ struct tw4<double> {
     using t = double4;
 };
 
+// Table entries keep only w: a 64-bit shared read costs 2 wavefronts per warp
+// (a 128-bit one 4, even when broadcast); rot(w) = (-w.y, w.x) is one FMUL2.
 template <typename T>
 __device__ __forceinline__ Tw<T> load_tw(const typename tw4<T>::t* p)
 {
-    const typename tw4<T>::t v = *p;
     Tw<T> w;
-    w.lo.x = v.x;
-    w.lo.y = v.y;
-    w.hi.x = v.z;
-    w.hi.y = v.w;
+    w.lo = *reinterpret_cast<const typename cx<T>::t*>(p);
+    if constexpr (sizeof(T) == 4)
+        w.hi = mul2(swz(w.lo), make_float2(-1.f, 1.f));
+    else
+        w.hi = make_c<T>(-w.lo.y, w.lo.x);
     return w;
 }
 
@@ -116,6 +120,9 @@ __device__ __forceinline__ typename cx<T>::t cmul_tw(typename cx<T>::t v, const 
         return CONJ ? cmulc(v, w.lo) : cmul(v, w.lo);
     }
 }
+
+__device__ __forceinline__ void opaque(float2& v) { asm volatile("" : "+f"(v.x), "+f"(v.y)); }
+__device__ __forceinline__ void opaque(double2& v) { asm volatile("" : "+d"(v.x), "+d"(v.y)); }
 
 template <typename T>
 __device__ __forceinline__ Tw<T> make_twv(typename cx<T>::t w)
@@ -236,79 +243,85 @@ struct SyncGroup {
 
 // wreg (optional): per-thread twiddle bases, slot(s, i) = w_N^{jm N/(Ns p)};
 // when given, powers are formed in registers instead of reading the table.
-template <typename T, int N, bool INV, int K, class SIdx, class Sync = SyncCta, bool REGTW = false>
-__device__ __forceinline__ void fft_rows(typename cx<T>::t (&v)[K][8], typename cx<T>::t* buf0,
-                                         typename cx<T>::t* buf1, const SIdx& sidx,
-                                         const typename tw4<T>::t* tw, int t, int& xc,
-                                         const Sync& sync = Sync(), const Tw<T>* wreg = nullptr)
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f)
+{
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + 1, E>(f);
+    }
+}
+
+// Stage S of K simultaneous length-N transforms (compile-time stage, radix
+// and butterfly indices, so every register/twiddle index is a constant).
+template <typename T, int N, bool INV, int K, bool REGTW, int S, class SIdx, class Sync, class WReg>
+__device__ __forceinline__ void fft_stage(typename cx<T>::t (&v)[K][8], typename cx<T>::t* buf0,
+                                          typename cx<T>::t* buf1, const SIdx& sidx,
+                                          const typename tw4<T>::t* tw, int t, int& xc,
+                                          const Sync& sync, const WReg& wreg)
 {
     using T2 = typename cx<T>::t;
     using PL = Plan<N>;
     constexpr int TF = PL::TF;
+    constexpr int p = PL::radix(S);
+    constexpr int ns = PL::ns(S);
+    constexpr int G = 8 / p;
+    if constexpr (S > 0) {
+        static_for<0, G>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            if constexpr (REGTW && S == PL::NST - 1) {
+                // last stage (a distinct base per thread): powers of a register
+                // base instead of table reads
+                Tw<T> b = wreg[i];
+                T2 pw[8];
+                pw[1] = b.lo;
+                if constexpr (p > 2)
+                    pw[2] = cmul_tw<T, false>(b.lo, b);
+                if constexpr (p > 3)
+                    pw[3] = cmul_tw<T, false>(pw[2], b);
+                if constexpr (p > 4) {
+                    const Tw<T> b2 = make_twv<T>(pw[2]);
+                    pw[4] = cmul_tw<T, false>(pw[2], b2);
+                    pw[5] = cmul_tw<T, false>(pw[4], b);
+                    pw[6] = cmul_tw<T, false>(pw[4], b2);
+                    pw[7] = cmul_tw<T, false>(pw[4], make_twv<T>(pw[3]));
+                }
 #pragma unroll
-    for (int s = 0; s < PL::NST; ++s) {
-        const int p = PL::radix(s);
-        const int ns = PL::ns(s);
-        const int G = 8 / p;
-        if (s > 0) {
+                for (int r = 1; r < p; ++r) {
+                    const Tw<T> w = make_twv<T>(pw[r]);
 #pragma unroll
-            for (int i = 0; i < G; ++i) {
-                const int j = t + i * TF;
-                const int jm = j % ns;
-                if (REGTW && s == PL::NST - 1) {
-                    // last twiddled stage (Ns = N/p, a distinct base per thread):
-                    // powers of the register base instead of 4-wavefront table reads
-                    typename cx<T>::t pw[8];
-                    const Tw<T> b = wreg[i];
-                    pw[1] = b.lo;
-                    if (p > 2)
-                        pw[2] = cmul_tw<T, false>(b.lo, b);
-                    if (p > 3)
-                        pw[3] = cmul_tw<T, false>(pw[2], b);
-                    if (p > 4) {
-                        const Tw<T> b2 = make_twv<T>(pw[2]);
-                        pw[4] = cmul_tw<T, false>(pw[2], b2);
-                        pw[5] = cmul_tw<T, false>(pw[4], b);
-                        pw[6] = cmul_tw<T, false>(pw[4], b2);
-                        pw[7] = cmul_tw<T, false>(pw[4], make_twv<T>(pw[3]));
-                    }
+                    for (int k = 0; k < K; ++k)
+                        v[k][i + r * G] = cmul_tw<T, INV>(v[k][i + r * G], w);
+                }
+            } else {
+                const int jm = (t + i * TF) % ns;
 #pragma unroll
-                    for (int r = 1; r < p; ++r) {
-                        const Tw<T> w = make_twv<T>(pw[r]);
+                for (int r = 1; r < p; ++r) {
+                    const Tw<T> w = load_tw<T>(tw + PL::tw_off(S) + jm * (p - 1) + (r - 1));
 #pragma unroll
-                        for (int k = 0; k < K; ++k)
-                            v[k][i + r * G] = cmul_tw<T, INV>(v[k][i + r * G], w);
-                    }
-                } else {
-#pragma unroll
-                    for (int r = 1; r < p; ++r) {
-                        const Tw<T> w = load_tw<T>(tw + PL::tw_off(s) + jm * (p - 1) + (r - 1));
-#pragma unroll
-                        for (int k = 0; k < K; ++k)
-                            v[k][i + r * G] = cmul_tw<T, INV>(v[k][i + r * G], w);
-                    }
+                    for (int k = 0; k < K; ++k)
+                        v[k][i + r * G] = cmul_tw<T, INV>(v[k][i + r * G], w);
                 }
             }
+        });
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        if constexpr (p == 8)
+            butterfly<T, 8, INV>(v[k], 0);
+        else if constexpr (p == 4) {
+            butterfly<T, 4, INV>(v[k], 0);
+            butterfly<T, 4, INV>(v[k], 1);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                butterfly<T, 2, INV>(v[k], i);
         }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if (p == 8)
-                butterfly<T, 8, INV>(v[k], 0);
-            else if (p == 4) {
-#pragma unroll
-                for (int i = 0; i < 2; ++i)
-                    butterfly<T, 4, INV>(v[k], i);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    butterfly<T, 2, INV>(v[k], i);
-            }
-        }
-        if (s == PL::NST - 1)
-            break;  // last stage outputs are already in the row pattern
+    }
+    if constexpr (S < PL::NST - 1) {
         T2* buf = (xc++ & 1) ? buf1 : buf0;
-#pragma unroll
-        for (int i = 0; i < G; ++i) {
+        static_for<0, G>([&](auto I) {
+            constexpr int i = decltype(I)::value;
             const int j = t + i * TF;
             const int jm = j % ns;
             const int base = (j - jm) * p + jm;
@@ -317,14 +330,35 @@ __device__ __forceinline__ void fft_rows(typename cx<T>::t (&v)[K][8], typename 
 #pragma unroll
                 for (int k = 0; k < K; ++k)
                     buf[sidx(k, base + q * ns)] = v[k][i + q * G];
-        }
+        });
         sync();
 #pragma unroll
         for (int m = 0; m < 8; ++m)
 #pragma unroll
             for (int k = 0; k < K; ++k)
                 v[k][m] = buf[sidx(k, t + m * TF)];
+        fft_stage<T, N, INV, K, REGTW, S + 1>(v, buf0, buf1, sidx, tw, t, xc, sync, wreg);
     }
+}
+
+struct NoWReg {
+    template <typename I>
+    __device__ int operator[](I) const { return 0; }
+};
+
+// K simultaneous length-N transforms of the row pattern held in v[k][8].
+// buf0/buf1: ping-pong exchange buffers; sidx(k, pos) gives the element index
+// of (transform k, position pos) inside one buffer. xc counts exchanges across
+// calls so consecutive exchanges alternate buffers (one barrier each). wreg
+// (REGTW): per-thread twiddle bases indexed by Plan::slot(stage, butterfly).
+template <typename T, int N, bool INV, int K, class SIdx, class Sync = SyncCta, bool REGTW = false,
+          class WReg = NoWReg>
+__device__ __forceinline__ void fft_rows(typename cx<T>::t (&v)[K][8], typename cx<T>::t* buf0,
+                                         typename cx<T>::t* buf1, const SIdx& sidx,
+                                         const typename tw4<T>::t* tw, int t, int& xc,
+                                         const Sync& sync = Sync(), const WReg& wreg = WReg())
+{
+    fft_stage<T, N, INV, K, REGTW, 0>(v, buf0, buf1, sidx, tw, t, xc, sync, wreg);
 }
 
 // Shared-memory index maps (bank-conflict-free for the three access patterns
@@ -604,13 +638,15 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
     const int t = threadIdx.x % TF;
     // per-thread twiddle bases and split phase, loaded once (no table reads
     // inside the transforms)
-    constexpr int SL = PL::NST - 1;  // last stage: its twiddles come from registers
-    Tw<T> wreg[SL > 0 ? 8 / PL::radix(SL) : 1];
+    // per-thread twiddle bases of the last stage (powers in registers)
+    constexpr int SL = PL::NST - 1;
+    constexpr int NWR = SL > 0 ? 8 / PL::radix(SL) : 1;
+    Tw<T> wreg[NWR];
     if constexpr (SL > 0) {
         const T2* roots = static_cast<const T2*>(p.roots);
-        const int pr = PL::radix(SL), ns = PL::ns(SL);
+        constexpr int pr = PL::radix(SL), ns = PL::ns(SL);
 #pragma unroll
-        for (int i = 0; i < 8 / pr; ++i) {
+        for (int i = 0; i < NWR; ++i) {
             const int jm = (t + i * TF) % ns;
             wreg[i] = make_twv<T>(ldg_c(roots + jm * (N / (ns * pr))));
         }
@@ -750,7 +786,7 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
                 }
 #pragma unroll
             for (int c = 0; c < M; ++c)
-                fft_rows<T, N, false, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, true>(
+                fft_rows<T, N, false, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, true, Tw<T>[NWR]>(
                     *reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx, tw, t, xc, fsync, wreg);
             const T2* sb = static_cast<const T2*>(sp.data) + sp.branch_base[beta] + off[beta];
             const int64_t bst = sp.block_elems[beta];
@@ -799,6 +835,9 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
                     for (int c = 0; c < 3; ++c)
                         v[c][m] = x[c];
                 }
+                // compiler barrier: keeps ptxas from hoisting all 8 x 6 spectra
+                // loads ahead of the arithmetic (that alone spills)
+                asm volatile("" ::: "memory");
             }
             if (compressed) {
                 __syncthreads();  // everyone is done with the staged row
@@ -807,7 +846,7 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
             }
 #pragma unroll
             for (int c = 0; c < M; ++c)
-                fft_rows<T, N, true, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, true>(
+                fft_rows<T, N, true, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, true, Tw<T>[NWR]>(
                     *reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx, tw, t, xc, fsync, wreg);
         }
         if (valid) {

@@ -25,6 +25,7 @@
 #include <utility>
 
 #include "tsk_common.cuh"
+#include "tsk_tmem.cuh"
 
 namespace tsk {
 namespace wide {
@@ -197,15 +198,17 @@ struct Tw {
     typename cx<T>::t lo, hi;
 };
 
+// Tables keep only w (64-bit reads: 2 wavefronts per warp even when
+// broadcast, a 128-bit read costs 4); rot(w) = (-w.y, w.x) is one FMUL2.
 template <typename T>
-__device__ __forceinline__ Tw<T> load_tw(const typename tw4<T>::t* p)
+__device__ __forceinline__ Tw<T> load_tw(const typename cx<T>::t* p)
 {
-    const typename tw4<T>::t v = *p;
     Tw<T> w;
-    w.lo.x = v.x;
-    w.lo.y = v.y;
-    w.hi.x = v.z;
-    w.hi.y = v.w;
+    w.lo = *p;
+    if constexpr (sizeof(T) == 4)
+        w.hi = mul2(swz(w.lo), make_float2(-1.f, 1.f));
+    else
+        w.hi = make_c<T>(-w.lo.y, w.lo.x);
     return w;
 }
 
@@ -233,7 +236,7 @@ __device__ __forceinline__ typename cx<T>::t cmul_tw(typename cx<T>::t v, const 
 }
 
 template <typename T, int N, int R>
-__device__ void fill_tables(typename tw4<T>::t* tw, typename tw4<T>::t* ph,
+__device__ void fill_tables(typename cx<T>::t* tw, typename cx<T>::t* ph,
                             const typename cx<T>::t* __restrict__ roots,
                             const typename cx<T>::t* __restrict__ phase)
 {
@@ -243,11 +246,11 @@ __device__ void fill_tables(typename tw4<T>::t* tw, typename tw4<T>::t* ph,
         const int p = P::radix(s), ns = P::ns(s);
         for (int e = threadIdx.x; e < ns * (p - 1); e += blockDim.x) {
             const int jm = e / (p - 1), r = e % (p - 1) + 1;
-            tw[P::tw_off(s) + e] = make_tw<T>(ldg_c(roots + (r * jm * (N / (ns * p))) % N));
+            tw[P::tw_off(s) + e] = ldg_c(roots + (r * jm * (N / (ns * p))) % N);
         }
     }
     for (int k = threadIdx.x; k < N; k += blockDim.x)
-        ph[k] = make_tw<T>(ldg_c(phase + k));
+        ph[k] = ldg_c(phase + k);
 }
 
 // One length-N transform of the row pattern v[m] = x[t + m TF] (m < R) of one
@@ -255,7 +258,7 @@ __device__ void fill_tables(typename tw4<T>::t* tw, typename tw4<T>::t* ph,
 // conflict free), two barriers per exchange (single buffer).
 template <typename T, int N, int R, int W, bool INV>
 __device__ __forceinline__ void fft_col(typename cx<T>::t (&v)[R], typename cx<T>::t* buf,
-                                        const typename tw4<T>::t* tw, int t, int w)
+                                        const typename cx<T>::t* tw, int t, int w)
 {
     using T2 = typename cx<T>::t;
     using PL = Plan<N, R>;
@@ -315,96 +318,6 @@ __device__ __forceinline__ void fft_col(typename cx<T>::t (&v)[R], typename cx<T
     }
 }
 
-// ---- tensor memory (thread-private lanes) ----------------------------------
-
-__device__ __forceinline__ uint32_t tmem_alloc(uint32_t* slot, int cols)
-{
-    // one warp allocates; the base address lands in shared memory
-    if (threadIdx.x < 32) {
-        const unsigned sa = (unsigned)__cvta_generic_to_shared(slot);
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa),
-                     "r"(cols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    return *slot;
-}
-
-__device__ __forceinline__ void tmem_free(uint32_t base, int cols)
-{
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (threadIdx.x < 32)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols)
-                     : "memory");
-}
-
-// Store / load 32 consecutive 32-bit columns of this thread's lane.
-__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&r)[32])
-{
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
-        "%29, %30, %31, %32};" ::"r"(addr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
-        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
-        "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
-        "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
-        "r"(r[29]), "r"(r[30]), "r"(r[31])
-        : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&r)[32])
-{
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
-        "%29, %30, %31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(addr)
-        : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// Park / restore R complex values (2 or 4 words each) in this thread's lane.
-template <typename T, int R>
-__device__ __forceinline__ void tmem_park(uint32_t lane_base, const typename cx<T>::t (&v)[R])
-{
-    constexpr int WORDS = R * (int)sizeof(typename cx<T>::t) / 4;
-    static_assert(WORDS % 32 == 0, "park granularity is 32 words");
-#pragma unroll
-    for (int c = 0; c < WORDS / 32; ++c) {
-        uint32_t r[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-            r[i] = reinterpret_cast<const uint32_t*>(&v[0])[c * 32 + i];
-        tmem_st32(lane_base + c * 32, r);
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
-
-template <typename T, int R>
-__device__ __forceinline__ void tmem_restore(uint32_t lane_base, typename cx<T>::t (&v)[R])
-{
-    constexpr int WORDS = R * (int)sizeof(typename cx<T>::t) / 4;
-#pragma unroll
-    for (int c = 0; c < WORDS / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(lane_base + c * 32, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-            reinterpret_cast<uint32_t*>(&v[0])[c * 32 + i] = r[i];
-    }
-}
-
 // ---- K1 / K3 ------------------------------------------------------------------
 
 template <typename T, int N, int R, int W, int MODE>
@@ -416,9 +329,9 @@ __global__ void __launch_bounds__(N / R * W) k_wide(tsk_axis p)
     constexpr int TF = PL::TF;
     constexpr int NT = TF * W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T4* tw = reinterpret_cast<T4*>(smem_raw);
-    T4* ph = tw + PL::TW;
-    T2* buf = reinterpret_cast<T2*>(ph + N);
+    T2* tw = reinterpret_cast<T2*>(smem_raw);
+    T2* ph = tw + PL::TW;
+    T2* buf = ph + N;
     __shared__ uint32_t tmem_slot;
     fill_tables<T, N, R>(tw, ph, static_cast<const T2*>(p.roots), static_cast<const T2*>(p.phase));
     __syncthreads();
@@ -560,7 +473,7 @@ static int launch(const tsk_axis& a, cudaStream_t st)
     using T2 = typename cx<T>::t;
     if (G::NT > 1024 || a.inner % G::W != 0)
         return -1;
-    const size_t smem = 2 * sizeof(T2) * (Plan<N, G::R>::TW + N) + sizeof(T2) * N * G::W;
+    const size_t smem = sizeof(T2) * (Plan<N, G::R>::TW + N) + sizeof(T2) * N * G::W;
     if (smem > 227 * 1024)
         return -1;
     auto kern = k_wide<T, N, G::R, G::W, MODE>;
