@@ -132,9 +132,7 @@ def make_operator(T, cfg, part, nparts, device):
         # configs[4]: non-symmetric CN(0,1) lags scaled by 1/(1+|m|_2), seed 5
         import numpy as np
         g = T.Generator.random(levels, 5, 0.5, T.SYM_GENERAL)
-        # the ABI has no lag getter: regenerate the same draws host-side
-        from oracle import Oracle  # test infrastructure RNG restatement (bit-exact)
-        lags = Oracle().random_lags(levels, 5, 0.5, 0)
+        lags = g.lags()
         grids = np.meshgrid(*[np.arange(-(n - 1), n) for n in levels], indexing="ij")
         r = np.sqrt(sum(gr.astype(np.float64) ** 2 for gr in grids)).reshape(-1)
         lags = lags / (1.0 + r)
@@ -186,10 +184,14 @@ def run_b200(args):
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream(dev)
 
+    from paper_2406_17981_b200 import partition
+
+    partition.check_world(world, d)
+
     def step():
         op.apply_device(x, y, stream)
         if world > 1:
-            dist.reduce(y, dst=0, op=dist.ReduceOp.SUM)
+            partition.reduce_partials(y, dst=0)  # NCCL over NVLink
 
     for _ in range(args.warmup):
         step()

@@ -57,6 +57,10 @@ ts_status ts_block_generator_create(int32_t d, const int64_t* levels, int32_t m,
 ts_status ts_block_generator_dyadic(int32_t d, const int64_t* levels, double k, double self_re,
                                     double self_im, ts_block_generator** out);
 
+/* Copy a scalar generator's lag tensor (interleaved, prod(2 n_l - 1) complex)
+ * into out — the reference ABI has no lag getter. */
+ts_status ts_generator_get_lags(const ts_generator* g, double* out);
+
 /* Wrap a scalar generator (m = 1); per-axis signs from its symmetry mode. */
 ts_status ts_block_generator_from_scalar(const ts_generator* g, ts_block_generator** out);
 

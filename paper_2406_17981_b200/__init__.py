@@ -42,7 +42,7 @@ EXTENSION_SYMBOLS = [
     "ts_block_generator_create", "ts_block_generator_dyadic", "ts_block_generator_from_scalar",
     "ts_block_generator_components", "ts_block_generator_destroy", "ts_split_options_default",
     "ts_operator_create_split_ex", "ts_operator_apply_device", "ts_operator_get_info",
-    "ts_device_count", "ts_operator_profile_device",
+    "ts_device_count", "ts_operator_profile_device", "ts_generator_get_lags",
 ]
 LAUNCHER_SYMBOLS = [
     "tsk_fwd_split", "tsk_inv_merge", "tsk_leaf_pair", "tsk_embed_generator", "tsk_embed_dyadic",
@@ -137,6 +137,7 @@ def _load():
     L.ts_block_generator_dyadic.argtypes = [C.c_int32, _i64p, C.c_double, C.c_double, C.c_double,
                                             C.POINTER(_vp)]
     L.ts_block_generator_from_scalar.argtypes = [_vp, C.POINTER(_vp)]
+    L.ts_generator_get_lags.argtypes = [_vp, _dp]
     L.ts_block_generator_components.argtypes = [_vp]
     L.ts_block_generator_destroy.argtypes = [_vp]
     L.ts_split_options_default.argtypes = [C.POINTER(TsSplitOptions)]
@@ -224,6 +225,11 @@ class Generator:
         out = np.zeros(self.dims, np.int64)
         _ok(lib.ts_generator_levels(self._h, out.ctypes.data_as(_i64p)))
         return [int(v) for v in out]
+
+    def lags(self):
+        out = np.zeros(int(np.prod([2 * n - 1 for n in self.levels])), np.complex128)
+        _ok(lib.ts_generator_get_lags(self._h, out.ctypes.data_as(_dp)))
+        return out
 
     def naive_matvec(self, v, cap=4096):
         s = int(np.prod(self.levels))

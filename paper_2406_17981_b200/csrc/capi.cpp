@@ -314,6 +314,14 @@ ts_status ts_block_generator_dyadic(int32_t d, const int64_t* levels, double k, 
     });
 }
 
+ts_status ts_generator_get_lags(const ts_generator* g, double* out)
+{
+    return guarded([&] {
+        need(g && out);
+        std::memcpy(static_cast<void*>(out), g->g.lags.data(), g->g.lags.size() * sizeof(cplx));
+    });
+}
+
 ts_status ts_block_generator_from_scalar(const ts_generator* g, ts_block_generator** out)
 {
     return guarded([&] {

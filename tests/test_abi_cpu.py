@@ -1,0 +1,184 @@
+"""CPU tests of the drop-in C ABI (libtoesplit.so.1): the library loads, exports
+every function the public headers declare, and its host-side services behave
+like the reference C API (proj/tests/capi/test_capi.cpp). No kernel is
+launched here; without a GPU the split engine must fail loudly.
+"""
+import os
+import re
+import tempfile
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2406_17981_b200 as T
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+O = oracle.Oracle()
+
+
+def _declared(header):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(tsk?_[a-z0-9_]+)\s*\(", text)))
+
+
+def _exported():
+    import subprocess
+
+    out = subprocess.run(["nm", "-D", "--defined-only", T.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    return {line.split()[-1] for line in out.splitlines() if " T " in line}
+
+
+@pytest.mark.parametrize("header", ["toesplit.h", "toesplit_ext.h", "tsk_launch.h"])
+def test_every_declared_symbol_is_exported(header):
+    declared = _declared(header)
+    assert declared, header
+    missing = [s for s in declared if s not in _exported()]
+    assert not missing, missing
+
+
+def test_reference_abi_is_complete():
+    # the 22 functions of the reference header (ref toesplit.h:84-156)
+    assert len(T.REFERENCE_SYMBOLS) == 22
+    assert set(T.REFERENCE_SYMBOLS) == set(_declared("toesplit.h"))
+    exported = _exported()
+    for s in T.REFERENCE_SYMBOLS + T.EXTENSION_SYMBOLS + T.LAUNCHER_SYMBOLS:
+        assert s in exported, s
+
+
+def test_only_abi_symbols_exported():
+    # the version script keeps C++ internals local
+    assert all(s.startswith("ts") for s in _exported()), sorted(_exported())[:5]
+
+
+def test_version_and_status_names():
+    assert T.version() == "1.0.0"
+    assert T.lib.ts_status_name(0).decode() == "ok"
+    assert T.lib.ts_status_name(3).decode() == "symmetry violation"
+    assert T.lib.ts_status_name(8).decode() == "internal error"
+
+
+@pytest.mark.parametrize("levels", [[7], [3, 4], [5, 4, 3], [2, 2, 2, 3]])
+@pytest.mark.parametrize("sym", [0, 1, 2])
+def test_instances_bit_exact_with_reference_rng(levels, sym):
+    # SplitMix64 / Box-Muller / symmetrize (ref instance.cpp) -> GPU inputs
+    # equal oracle inputs
+    v = T.random_vector(levels, 9, 0.5)
+    assert np.array_equal(v, O.random_vector(levels, 9, 0.5))
+    g = T.Generator.random(levels, 9, 1.0, sym)
+    lags = O.random_lags(levels, 9, 1.0, sym)
+    y = g.naive_matvec(v, cap=10000)
+    assert np.array_equal(y, O.naive(levels, lags, v, cap=10000))
+
+
+def test_large_vector_rng_parallel_split_is_exact():
+    # the chunked (multi-threaded) draw equals the sequential stream
+    lv = [3, 40, 40, 40]
+    assert np.array_equal(T.random_vector(lv, 4, 0.5), O.random_vector(lv, 4, 0.5))
+
+
+def test_json_fixture_round_trip_and_errors():
+    g = T.Generator.random([2, 3], 555, 1.5, T.SYM_SYMMETRIC)
+    with tempfile.TemporaryDirectory() as td:
+        p = os.path.join(td, "g.json")
+        g.to_json_file(p)
+        g2 = T.Generator.from_json_file(p)
+        assert g2.levels == [2, 3]
+        v = T.random_vector([2, 3], 1)
+        assert np.array_equal(g.naive_matvec(v), g2.naive_matvec(v))
+        bad = os.path.join(td, "bad.json")
+        for text, code in [("{", T.TS_ERR_IO), ('{"levels":[2]}', T.TS_ERR_IO),
+                           ('{"levels":[2],"lags":[[1,0],[2,0],[3,0]],"symmetry":"symmetric"}',
+                            T.TS_ERR_SYMMETRY),
+                           ('{"levels":[2],"lags":[[-3,0],[2,0],[3,0]],"symmetry":"skew"}',
+                            T.TS_ERR_SYMMETRY)]:
+            open(bad, "w").write(text)
+            with pytest.raises(T.TsError) as e:
+                T.Generator.from_json_file(bad)
+            assert e.value.code == code
+        open(bad, "w").write('{"levels":[2],"lags":[[-3,0],[0,0],[3,0]],"symmetry":"skew"}')
+        T.Generator.from_json_file(bad)
+        with pytest.raises(T.TsError) as e:
+            T.Generator.from_json_file(os.path.join(td, "missing.json"))
+        assert e.value.code == T.TS_ERR_IO
+
+
+def test_reference_json_is_readable():
+    # a fixture written by the reference itself (nlohmann dump) loads here
+    if not os.path.exists(oracle.REF_PATH):
+        pytest.skip("oracle/_ref not built")
+    R = oracle.RefLib()
+    g = R.generator([3, 2], seed=5, symmetry=1)
+    with tempfile.TemporaryDirectory() as td:
+        p = os.path.join(td, "ref.json")
+        assert R.L.ts_generator_to_json_file(g, p.encode()) == 0
+        ours = T.Generator.from_json_file(p)
+        v = T.random_vector([3, 2], 2)
+        assert np.array_equal(ours.naive_matvec(v), R.naive(g, v))
+    R.destroy_gen(g)
+
+
+def test_error_codes_match_reference_capi():
+    # test_capi.cpp:101-126
+    import ctypes as C
+
+    h = C.c_void_p()
+    assert T.lib.ts_generator_create(1, None, None, 0, None) == T.TS_ERR_INVALID_ARGUMENT
+    assert len(T.lib.ts_last_error()) > 0
+    with pytest.raises(T.TsError) as e:
+        T.Generator.create([2], np.array([1, 2, 3]), T.SYM_SYMMETRIC)
+    assert e.value.code == T.TS_ERR_SYMMETRY
+    g = T.Generator.create([2], np.array([1, 2, 3]), T.SYM_GENERAL)
+    with pytest.raises(T.TsError) as e:
+        g.naive_matvec(np.array([1, 0]), cap=1)
+    assert e.value.code == T.TS_ERR_CAP_EXCEEDED
+    assert T.lib.ts_generator_random(0, None, 1, 1.0, 0, C.byref(h)) == T.TS_ERR_INVALID_ARGUMENT
+    lv = (C.c_int64 * 1)(4)
+    assert T.lib.ts_random_vector(1, lv, 1, -1.0, (C.c_double * 8)()) == T.TS_ERR_INVALID_ARGUMENT
+    # success clears the detail string
+    T.random_vector([2], 1)
+    assert T.lib.ts_last_error() == b""
+
+
+def test_predict_values():
+    c = T.predict(3, 1024)
+    assert abs(c["r_m"] - 4 / 3) <= 1e-12 and abs(c["r_m_sym"] - 9 / 5) <= 1e-12
+    assert abs(c["r_c_asymptote"] - 12 / 7) <= 1e-12
+    assert abs(T.predict(6, 1024)["r_m_sym"] - 65 / 8) <= 1e-12
+    ref = O.predict(3, 512)
+    ours = T.predict(3, 512)
+    for k in ("c_embed", "c_split", "r_c", "r_m", "r_m_sym"):
+        assert ours[k] == ref[k]
+    for bad in ((0, 1024), (2, 1)):
+        with pytest.raises(T.TsError) as e:
+            T.predict(*bad)
+        assert e.value.code == T.TS_ERR_INVALID_ARGUMENT
+
+
+def test_block_generator_validation_on_host():
+    # per-axis signs validated exactly (ref generator.cpp:38-62 generalised)
+    levels = [3, 4, 2]
+    lag = O.dyadic_lags(levels, 0, 1)
+    bg = T.BlockGenerator.create(levels, 1, [0], [lag], [[-1, -1, 1]])
+    assert bg.components == 1
+    with pytest.raises(T.TsError) as e:
+        T.BlockGenerator.create(levels, 1, [0], [lag], [[1, 1, 1]])
+    assert e.value.code == T.TS_ERR_SYMMETRY
+    with pytest.raises(T.TsError):
+        T.BlockGenerator.create(levels, 2, [0, 1, 1, 5], [lag, lag], [[0] * 3, [0] * 3])
+    assert T.BlockGenerator.dyadic([8, 8, 8]).components == 3
+    with pytest.raises(T.TsError):
+        T.BlockGenerator.dyadic([8, 8])
+
+
+@pytest.mark.skipif(T.device_count() > 0, reason="a GPU is present")
+def test_split_engine_fails_loudly_without_gpu():
+    g = T.Generator.random([4, 4], 1)
+    for make in (lambda: T.Operator.split(g), lambda: T.Operator.embed(g),
+                 lambda: T.Operator.split_ex(T.BlockGenerator.dyadic([4, 4, 4]))):
+        with pytest.raises(T.TsError) as e:
+            make()
+        assert e.value.code == T.TS_ERR_RESOURCE
+        assert "GPU" in e.value.detail or "CUDA" in e.value.detail

@@ -1,0 +1,280 @@
+"""CPU tests of the oracle (test infrastructure): it must reproduce the
+reference's own known answers, the golden vectors produced by the unmodified
+reference build (tests/golden/make_golden.py), and — when oracle/_ref is built
+— the reference library itself, bit for bit on the same FFT.
+
+Reference tests mirrored (paths relative to /root/reference/proj):
+  tests/unit/test_fft.cpp, test_kernel.cpp, test_engine_split.cpp,
+  tests/capi/test_capi.cpp, tests/acceptance/acceptance_main.cpp.
+"""
+import itertools
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import SYM_GENERAL, SYM_SKEW, SYM_SYMMETRIC, max_rel, rel_l2
+
+O = oracle.Oracle()
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+SYMS = [SYM_GENERAL, SYM_SYMMETRIC, SYM_SKEW]
+
+
+def _direct_dft(x, inverse=False):
+    n = len(x)
+    k = np.arange(n)
+    w = np.exp((2j if inverse else -2j) * np.pi * np.outer(k, k) / n)
+    y = w @ x
+    return y / n if inverse else y
+
+
+def _split(levels, sym, seed, variance=1.0, s0=0j):
+    lags = O.random_lags(levels, seed, variance, sym)
+    v = O.random_vector(levels, seed, variance)
+    comp = sym == SYM_SYMMETRIC or (sym == SYM_SKEW and s0 == 0)
+    signs = oracle.axis_signs(len(levels), sym)
+    blocks = O.precompute(levels, lags, s0, comp, signs)
+    return lags, v, blocks, comp, signs
+
+
+# ---- FFT provider contract (test_fft.cpp) ---------------------------------
+
+def test_fft_known_answers():
+    # test_fft.cpp:12-40
+    assert np.allclose(O.fft_axis([2], [1, 0], 0), [1, 1])
+    assert np.allclose(O.fft_axis([2], [0, 1], 0), [1, -1])
+    assert np.allclose(O.fft_axis([2], [1, 1], 0, inverse=True), [1, 0])
+    assert np.allclose(O.fft_axis([2], [2, 0], 0, inverse=True), [1, 1])
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 7, 8, 12, 13, 16, 30, 64, 97, 128])
+def test_fft_vs_direct_dft(n):
+    # test_fft.cpp:66-80 (including primes), 1e-12
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    assert max_rel(O.fft_axis([n], x, 0), _direct_dft(x)) <= 1e-12
+    assert max_rel(O.fft_axis([n], x, 0, inverse=True), _direct_dft(x, True)) <= 1e-12
+
+
+def test_fft_round_trip_all_axes():
+    # test_fft.cpp:42-64 ({2..9}^d round trips, sampled)
+    rng = np.random.default_rng(0)
+    for shape in itertools.product([2, 3, 5, 9], repeat=2):
+        x = rng.standard_normal(int(np.prod(shape))) + 1j * rng.standard_normal(int(np.prod(shape)))
+        for a in range(2):
+            y = O.fft_axis(shape, O.fft_axis(shape, x, a), a, inverse=True)
+            assert max_rel(y, x) <= 1e-12
+
+
+def test_phase_and_split_identity():
+    # test_fft.cpp:82-122: DFT(P v) are the odd coefficients of DFT([v, 0])
+    pv = O.phase_axis([2], [0, 1], 0)
+    assert abs(pv[1] - (-1j)) < 1e-15
+    assert np.allclose(O.fft_axis([2], pv, 0), [-1j, 1j])
+    rng = np.random.default_rng(7)
+    for n in range(2, 17):
+        v = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        even = O.fft_axis([n], v, 0)
+        odd = O.fft_axis([n], O.phase_axis([n], v, 0), 0)
+        pad = np.fft.fft(np.concatenate([v, np.zeros(n)]))
+        scale = np.max(np.abs(pad))
+        assert np.max(np.abs(pad[0::2] - even)) / scale <= 1e-12
+        assert np.max(np.abs(pad[1::2] - odd)) / scale <= 1e-12
+
+
+# ---- spectra (test_kernel.cpp) --------------------------------------------
+
+def test_embedded_layout_and_parity_blocks():
+    # test_kernel.cpp:72-126: T = [[1,2],[3,1]] -> column [1,3,0,2];
+    # DFT = [6, 1-i, -4, 1+i]: even block [6,-4], odd block [1-i, 1+i]
+    lags = np.array([2, 1, 3], np.complex128)
+    assert np.allclose(O.embed_generator([2], lags), [1, 3, 0, 2])
+    assert np.allclose(O.embed_generator([2], lags, s0=9 + 9j), [1, 3, 9 + 9j, 2])
+    blocks = O.precompute([2], lags)
+    assert np.allclose(blocks[:2], [6, -4]) and np.allclose(blocks[2:], [1 - 1j, 1 + 1j])
+
+
+def test_symmetric_n2_dft_and_compression():
+    # test_kernel.cpp:180-200: DFT([a, b, 0, b]) = [a+2b, a, a-2b, a]
+    a, b = 2 + 1j, -1 + 3j
+    lags = np.array([b, a, b])
+    full = O.precompute([2], lags, 0j, False, [1])
+    assert np.allclose(full, [a + 2 * b, a - 2 * b, a, a])
+    packed = O.precompute([2], lags, 0j, True, [1])
+    assert packed.size == 3  # n + 1
+    assert np.allclose(packed, [a + 2 * b, a - 2 * b, a])
+
+
+def test_skew_zeros_and_compression_validation():
+    # test_kernel.cpp:202-210, 263-282
+    lags = O.random_lags([4], 77, 1.0, SYM_SKEW)
+    full = O.precompute([4], lags, 0j, False, [-1])
+    scale = np.max(np.abs(full))
+    assert abs(full[0]) <= 1e-12 * scale and abs(full[2]) <= 1e-12 * scale
+    with pytest.raises(oracle.OracleError) as e:
+        O.precompute([4], lags, 1 + 0j, True, [-1])  # nonzero skew padding
+    assert e.value.code == 3
+    with pytest.raises(oracle.OracleError):
+        O.precompute([4], O.random_lags([4], 9, 1.0, 0), 0j, True, [1])
+
+
+@pytest.mark.parametrize("levels", [[4, 4], [3, 4], [5], [2, 3, 4]])
+@pytest.mark.parametrize("sym", [SYM_SYMMETRIC, SYM_SKEW])
+def test_compressed_counts_and_equality(levels, sym):
+    # test_kernel.cpp:212-232: stored <= prod(n+1), same matvec
+    lags, v, full, _, signs = _split(levels, sym, 123)
+    full = O.precompute(levels, lags, 0j, False, signs)
+    packed = O.precompute(levels, lags, 0j, True, signs)
+    assert packed.size <= int(np.prod([n + 1 for n in levels]))
+    y_full = O.split_apply(levels, full, v, False, signs)
+    y_pack = O.split_apply(levels, packed, v, True, signs)
+    assert max_rel(y_pack, y_full) <= 1e-12
+
+
+# ---- split engine (test_engine_split.cpp) ---------------------------------
+
+def test_worked_2x2_and_counters():
+    # test_engine_split.cpp:27-39
+    lags = np.array([2, 1, 3], np.complex128)
+    blocks = O.precompute([2], lags)
+    y, c = O.split_apply([2], blocks, np.array([1, 1], np.complex128), counters=True)
+    assert np.allclose(y, [3, 4], atol=1e-12)
+    assert list(c) == [2, 2, 4, 4, 4]
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 4])
+def test_counter_contract(d):
+    # test_engine_split.cpp:156-206
+    levels = [3] * d
+    s = 3 ** d
+    _, v, blocks, comp, signs = _split(levels, SYM_GENERAL, 7)
+    _, c = O.split_apply(levels, blocks, v, comp, signs, counters=True)
+    assert c[0] == c[1] == 2 ** (d + 1) - 2
+    assert c[2] == 2 ** d * s and c[3] == 2 * (2 ** d - 1) * s and c[4] == (d + 1) * s
+
+
+@pytest.mark.parametrize("levels", [[2], [5], [3, 4], [2, 6], [2, 3, 4], [3, 3, 3]])
+@pytest.mark.parametrize("sym", SYMS)
+def test_split_vs_dense_and_embed(levels, sym):
+    # test_engine_split.cpp:118-138 / acceptance criterion 1
+    for seed in (1, 2, 3):
+        lags, v, blocks, comp, signs = _split(levels, sym, seed)
+        y = O.split_apply(levels, blocks, v, comp, signs)
+        assert max_rel(y, O.naive(levels, lags, v)) <= 1e-10
+        assert max_rel(y, O.embed_apply(levels, lags, v)) <= 1e-12
+
+
+def test_padding_independence_and_linearity():
+    levels = [3, 4]
+    lags = O.random_lags(levels, 42, 1.0, 0)
+    v = O.random_vector(levels, 42, 1.0)
+    y0 = O.split_apply(levels, O.precompute(levels, lags), v)
+    for s0 in (1 + 0j, 7 + 3j):
+        assert max_rel(O.split_apply(levels, O.precompute(levels, lags, s0), v), y0) <= 1e-12
+    u = O.random_vector(levels, 1, 1.0)
+    w = O.random_vector(levels, 2, 1.0)
+    b = O.precompute(levels, lags)
+    a1, a2 = 0.7 - 0.3j, -1.2 + 0.4j
+    lhs = O.split_apply(levels, b, a1 * u + a2 * w)
+    rhs = a1 * O.split_apply(levels, b, u) + a2 * O.split_apply(levels, b, w)
+    assert max_rel(lhs, rhs) <= 1e-12
+
+
+@pytest.mark.parametrize("nparts", [2, 4, 8])
+def test_partitions_sum_to_full(nparts):
+    # branch partition (multi-GPU split): sum of subtree partials == y
+    levels = [4, 3, 5]
+    for sym in (SYM_GENERAL, SYM_SYMMETRIC):
+        _, v, blocks, comp, signs = _split(levels, sym, 5)
+        y = O.split_apply(levels, blocks, v, comp, signs)
+        acc = sum(O.split_apply_partial(levels, blocks, v, p, nparts, comp, signs)
+                  for p in range(nparts))
+        assert rel_l2(acc, y) <= 1e-13
+
+
+def test_per_axis_signs_dyadic_matches_reference_composition():
+    # the B200 extension (per-axis parity compression of all 6 components)
+    # equals the reference's composition (G_ii symmetric, G_ij general)
+    levels = [5, 6, 4]
+    s = int(np.prod(levels))
+    x = O.random_vector([3] + levels, 2, 0.5)
+    xs = [x[i * s:(i + 1) * s] for i in range(3)]
+    ya = np.concatenate(O.dyadic_apply(levels, xs, mode="ref"))
+    yb = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+    assert rel_l2(ya, yb) <= 1e-13
+    for i in range(3):
+        for j in range(3):
+            lags = O.dyadic_lags(levels, i, j)
+            signs = [(-1) ** ((i == a) + (j == a)) for a in range(3)]
+            assert O.validate_symmetry(levels, lags, signs) == 0
+
+
+def test_predict_values():
+    # test_capi.cpp:164-176
+    p = O.predict(3, 1024)
+    assert abs(p["r_m"] - 4 / 3) <= 1e-12 and abs(p["r_m_sym"] - 9 / 5) <= 1e-12
+    assert abs(p["r_c_asymptote"] - 12 / 7) <= 1e-12
+    assert abs(O.predict(6, 1024)["r_m_sym"] - 65 / 8) <= 1e-12
+    with pytest.raises(oracle.OracleError):
+        O.predict(0, 1024)
+
+
+# ---- golden vectors from the unmodified reference --------------------------
+
+def test_golden_c0_reference_outputs():
+    g = np.load(os.path.join(GOLD, "c0_16cubed.npz"))
+    levels = [16, 16, 16]
+    x = O.random_vector(levels, 1, 0.5)
+    assert np.array_equal(x, g["x"])  # bit-exact RNG (instance.cpp)
+    lags = O.random_lags(levels, 0, 0.5, SYM_GENERAL)
+    assert np.array_equal(lags[:8], g["lags_head"]) and lags.sum() == g["lags_sum"]
+    blocks = O.precompute(levels, lags)
+    y, c = O.split_apply(levels, blocks, x, counters=True)
+    assert rel_l2(y, g["y_split_ref"]) <= 1e-14
+    assert max_rel(y, g["y_naive_ref"]) <= 1e-10
+    assert list(c[:5]) == list(g["counters"][:5])
+
+
+@pytest.mark.parametrize("name", ["sym_345", "skew_444", "gen_prime", "gen_d4"])
+def test_golden_scalar_cases(name):
+    g = np.load(os.path.join(GOLD, "scalar_cases.npz"))
+    levels = [int(n) for n in g[name + "_levels"]]
+    sym, seed = int(g[name + "_sym"]), int(g[name + "_seed"])
+    lags, v, blocks, comp, signs = _split(levels, sym, seed)
+    assert np.array_equal(v, g[name + "_x"])
+    assert rel_l2(O.split_apply(levels, blocks, v, comp, signs), g[name + "_y"]) <= 1e-14
+    assert rel_l2(O.embed_apply(levels, lags, v), g[name + "_ye"]) <= 1e-13
+
+
+def test_golden_dyadic_reference_composition():
+    g = np.load(os.path.join(GOLD, "dyadic_6cubed.npz"))
+    levels = [6, 6, 6]
+    s = 216
+    assert np.array_equal(O.random_vector([3] + levels, 2, 0.5), g["x"])
+    xs = [g["x"][i * s:(i + 1) * s] for i in range(3)]
+    assert rel_l2(np.concatenate(O.dyadic_apply(levels, xs, mode="ref")), g["y"]) <= 1e-14
+    assert rel_l2(np.concatenate(O.dyadic_apply(levels, xs, mode="signs")), g["y"]) <= 1e-13
+
+
+# ---- live cross-check against the reference build --------------------------
+
+@pytest.mark.skipif(not os.path.exists(oracle.REF_PATH), reason="oracle/_ref not built")
+def test_live_reference_sweep():
+    # acceptance criterion 1 (sampled): same inputs, outputs, counters
+    R = oracle.RefLib()
+    for d in (1, 2, 3):
+        for levels in itertools.product([2, 3, 4, 5], repeat=d):
+            levels = list(levels)
+            for sym in SYMS:
+                seed = sum(levels) + sym
+                lags, v, blocks, comp, signs = _split(levels, sym, seed)
+                y, c = O.split_apply(levels, blocks, v, comp, signs, counters=True)
+                gen = R.generator(levels, seed=seed, symmetry=sym)
+                op = R.split(gen)
+                yr, m = R.apply(op, R.random_vector(levels, seed), metrics=True)
+                assert rel_l2(y, yr) <= 1e-15
+                assert [m.fft_forward, m.diag_mults, m.phase_mults, m.peak_live_elems] == \
+                    [c[0], c[2], c[3], c[4]]
+                R.destroy_op(op)
+                R.destroy_gen(gen)
