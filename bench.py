@@ -437,7 +437,7 @@ def run_reference(args):
     base["value"] = value
     line = {
         "metric": METRIC, "impl": "reference", "value": value, "unit": "MVM/s",
-        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "n_gpus": args.gpus, "host_cores": os.cpu_count(), "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (reference SplitMix64/Box-Muller x, analytic dyadic kernel)",
         "config": {"workload": f"BASELINE.json configs[{cidx}] on host cores (sampled)",
