@@ -15,6 +15,7 @@ extern "C" int tsk_wide_fwd_split(const tsk_axis* a, void* stream);
 extern "C" int tsk_wide_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_fast_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_fast_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
+extern "C" int tsk_leaf1_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
 
 static bool env_flag(const char* name)
 {
@@ -26,6 +27,15 @@ static bool no_wide()
     static int v = -1;
     if (v < 0)
         v = env_flag("TSK_NO_WIDE") ? 1 : 0;
+    return v == 1;
+}
+
+// TSK_NO_LEAF1=1 selects the 3-components-per-thread leaf kernel (A/B).
+static bool no_leaf1()
+{
+    static int v = -1;
+    if (v < 0)
+        v = env_flag("TSK_NO_LEAF1") ? 1 : 0;
     return v == 1;
 }
 
@@ -69,7 +79,10 @@ extern "C" int tsk_inv_merge(const tsk_axis* a, void* stream)
 extern "C" int tsk_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream)
 {
     if (!generic_only()) {
-        const int e = tsk_fast_leaf_pair(a, sp, stream);
+        int e = no_leaf1() ? -1 : tsk_leaf1_pair(a, sp, stream);
+        if (e != -1)
+            return e;
+        e = tsk_fast_leaf_pair(a, sp, stream);
         if (e != -1)
             return e;
     }

@@ -19,6 +19,7 @@
 // tensor.cpp:227-254, engine_split.cpp:13-37, kernel.cpp:126-219).
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -347,6 +348,11 @@ __device__ __forceinline__ void fft_stage(typename cx<T>::t (&v)[K][8], typename
     }
 }
 
+// leaf pass: last-stage twiddles from register powers (true) or the table
+#ifndef LEAF_REGTW
+#define LEAF_REGTW false
+#endif
+
 struct NoWReg {
     template <typename I>
     __device__ int operator[](I) const { return 0; }
@@ -608,9 +614,18 @@ __device__ __forceinline__ void matvec3(typename cx<T>::t (&x)[3], const typenam
 // fibers. Components are transformed one after another through a single pair
 // of exchange buffers; the m x m multiply happens in registers. The leaf
 // parities along the last axis are even (beta 0) and odd (beta 1).
-template <typename T, int N, int M, int G>
-__global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(tsk_axis p, tsk_spectra sp)
+template <typename T, int N, int M, int G, bool DBG = false>
+__global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(tsk_axis p, tsk_spectra sp,
+                                                                             unsigned long long* dbg = nullptr)
 {
+    // DBG: per-phase clock64 accounting of thread 0 (tools: TSK_PHASE_DEBUG=1)
+    unsigned long long dacc[12] = {0}, dlast = 0;
+#define TSK_T(i)                                      \
+    if (DBG && threadIdx.x == 0) {                    \
+        const unsigned long long c_ = clock64();      \
+        dacc[i] += c_ - dlast;                        \
+        dlast = c_;                                   \
+    }
     using T2 = typename cx<T>::t;
     using T4 = typename tw4<T>::t;
     using PL = Plan<N>;
@@ -692,6 +707,8 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
     T2* stash_me = stash + slot * N + t;
     int xc = 0;
 
+    if (DBG && threadIdx.x == 0)
+        dlast = clock64();
     for (int64_t tile = blockIdx.x; tile * G < units; tile += gridDim.x) {
         const int64_t u = tile * G + gi;
         bool valid = false;
@@ -703,9 +720,13 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
                 valid = g < p.outer;
                 off[0] = off[1] = g * N;
             } else {
-                const int64_t s2 = u % st2;
-                const int64_t s1 = (u / st2) % st1;
-                const int64_t r = u / (st2 * st1);
+                // unit -> (rest, s1, s2): 32-bit (units < 2^31), no 64-bit division
+                const uint32_t u32 = (uint32_t)u, st2u = (uint32_t)st2, st1u = (uint32_t)st1;
+                const uint32_t q2 = u32 / st2u;
+                const int64_t s2 = u32 - q2 * st2u;
+                const uint32_t q1 = q2 / st1u;
+                const int64_t s1 = q2 - q1 * st1u;
+                const int64_t r = q1;
                 int64_t p1 = 0, p2 = 0;
                 const int c1 = A1 >= 0 ? orbit_members(n1, (bits >> A1) & 1u, s1, p1) : 1;
                 const int c2 = A2 >= 0 ? orbit_members(n2, (bits >> A2) & 1u, s2, p2) : 1;
@@ -762,6 +783,7 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
         // every member thread computed the same unit row; slot-0 threads hold it
         // whether or not their own fiber is valid (row offsets depend on the unit)
         stage(p.use_even ? 0 : 1);
+        TSK_T(0);
         T2 v[M][8];
 #pragma unroll
         for (int beta = 0; beta < 2; ++beta) {
@@ -791,61 +813,87 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
                         v[c][m] = phr.template apply<false>(x, m);
                     }
                 }
+            TSK_T(1 + 5 * beta);
 #pragma unroll
             for (int c = 0; c < M; ++c)
-                fft_rows<T, N, false, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, true, Tw<T>[NWR]>(
+                fft_rows<T, N, false, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, LEAF_REGTW, Tw<T>[NWR]>(
                     *reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx, tw, t, xc, fsync, wreg);
+            TSK_T(2 + 5 * beta);
             const T2* sb = static_cast<const T2*>(sp.data) + sp.branch_base[beta] + off[beta];
             const int64_t bst = sp.block_elems[beta];
             if (compressed) {
                 cp_async_wait_all();
                 __syncthreads();  // the staged row is complete and visible
             }
+            TSK_T(3 + 5 * beta);
+            constexpr int MB = 1;  // frequencies per spectra batch
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const int k = t + m * TF;
-                int kidx = k;
-                bool mir = false;
-                if (compressed) {
-                    // beta 0: even parity (stores 0..N/2), beta 1: odd (0..N/2-1)
-                    if (beta == 0) {
-                        mir = k > N / 2;
-                        kidx = mir ? N - k : k;
-                    } else {
-                        mir = k >= N / 2;
-                        kidx = mir ? N - 1 - k : k;
+            for (int mb = 0; mb < 8; mb += MB) {
+                int kidx[MB];
+                uint32_t ngs[MB];
+#pragma unroll
+                for (int mm = 0; mm < MB; ++mm) {
+                    const int k = t + (mb + mm) * TF;
+                    int ki = k;
+                    bool mir = false;
+                    if (compressed) {
+                        // beta 0: even parity (stores 0..N/2), beta 1: odd (0..N/2-1)
+                        if (beta == 0) {
+                            mir = k > N / 2;
+                            ki = mir ? N - k : k;
+                        } else {
+                            mir = k >= N / 2;
+                            ki = mir ? N - 1 - k : k;
+                        }
                     }
+                    kidx[mm] = ki;
+                    ngs[mm] = neg ^ (mir ? lastneg : 0u);
                 }
-                const uint32_t ng = neg ^ (mir ? lastneg : 0u);
                 if (M == 1) {
-                    T2 sv = make_c<T>(0, 0);
-                    if (compressed)
-                        sv = stg[kidx];
-                    else if (valid)
-                        sv = ldg_c(sb + kidx);
-                    sv = flip_sign(sv, ng & 1u);
-                    v[0][m] = cmul(v[0][m], sv);
-                } else {
-                    T2 sv[6];
+                    T2 sv[MB];
 #pragma unroll
-                    for (int uu = 0; uu < 6; ++uu) {
-                        T2 s = make_c<T>(0, 0);
+                    for (int mm = 0; mm < MB; ++mm) {
+                        sv[mm] = make_c<T>(0, 0);
                         if (compressed)
-                            s = stg[uu * LROW + kidx];
+                            sv[mm] = stg[kidx[mm]];
                         else if (valid)
-                            s = ldg_c(sb + uu * bst + kidx);
-                        sv[uu] = flip_sign(s, (ng >> uu) & 1u);
+                            sv[mm] = ldg_c(sb + kidx[mm]);
                     }
-                    T2 x[3] = {v[0][m], v[1][m], v[2][m]};
-                    matvec3<T>(x, sv);
 #pragma unroll
-                    for (int c = 0; c < 3; ++c)
-                        v[c][m] = x[c];
+                    for (int mm = 0; mm < MB; ++mm)
+                        v[0][mb + mm] = cmul(v[0][mb + mm], flip_sign(sv[mm], ngs[mm] & 1u));
+                } else {
+                    // 4 frequencies x 6 unique components loaded together, then
+                    // four 3x3 products
+                    T2 sv[MB][6];
+#pragma unroll
+                    for (int mm = 0; mm < MB; ++mm)
+#pragma unroll
+                        for (int uu = 0; uu < 6; ++uu) {
+                            T2 sx = make_c<T>(0, 0);
+                            if (compressed)
+                                sx = stg[uu * LROW + kidx[mm]];
+                            else if (valid)
+                                sx = ldg_c(sb + uu * bst + kidx[mm]);
+                            sv[mm][uu] = sx;
+                        }
+#pragma unroll
+                    for (int mm = 0; mm < MB; ++mm) {
+#pragma unroll
+                        for (int uu = 0; uu < 6; ++uu)
+                            sv[mm][uu] = flip_sign(sv[mm][uu], (ngs[mm] >> uu) & 1u);
+                        T2 x[3] = {v[0][mb + mm], v[1][mb + mm], v[2][mb + mm]};
+                        matvec3<T>(x, sv[mm]);
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+                            v[c][mb + mm] = x[c];
+                    }
                 }
-                // compiler barrier: keeps ptxas from hoisting all 8 x 6 spectra
-                // loads ahead of the arithmetic (that alone spills)
+                // compiler barrier between the two halves: bounds the number of
+                // spectra values held in registers (all 48 at once spills)
                 asm volatile("" ::: "memory");
             }
+            TSK_T(4 + 5 * beta);
             if (compressed) {
                 __syncthreads();  // everyone is done with the staged row
                 if (beta == 0 && p.use_odd)
@@ -853,8 +901,9 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
             }
 #pragma unroll
             for (int c = 0; c < M; ++c)
-                fft_rows<T, N, true, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, true, Tw<T>[NWR]>(
+                fft_rows<T, N, true, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, LEAF_REGTW, Tw<T>[NWR]>(
                     *reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx, tw, t, xc, fsync, wreg);
+            TSK_T(5 + 5 * beta);
         }
         if (valid) {
             T2* yout = dst + g * N + t;
@@ -874,10 +923,14 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
                 }
         }
     }
+    if (DBG && threadIdx.x == 0 && dbg)
+        for (int i = 0; i < 12; ++i)
+            atomicAdd(dbg + i, dacc[i]);
+#undef TSK_T
 }
 
 template <typename T, int N, int M, int G>
-__global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf_ilp(tsk_axis p, tsk_spectra sp)
+__global__ void __launch_bounds__(N / 8 * 4 * G, 1) k_leaf_ilp(tsk_axis p, tsk_spectra sp, unsigned long long* = nullptr)
 {
     using T2 = typename cx<T>::t;
     using T4 = typename tw4<T>::t;
@@ -886,13 +939,13 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf_
     constexpr int S = 4 * G;  // fiber slots per CTA
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T4* twt = reinterpret_cast<T4*>(smem_raw);
-    T2* buf0 = reinterpret_cast<T2*>(twt + PL::TW);  // M x S x N, single buffer
-    T2* buf1 = buf0;
+    T2* buf0 = reinterpret_cast<T2*>(twt + PL::TW);  // M x S x N, ping-pong
+    T2* buf1 = buf0 + M * S * N;
     // compressed spectra: one branch's stored row of every unique component,
     // per unit, staged with cp.async while the forward transforms run
     constexpr int LROW = N / 2 + 1;
     constexpr int UM = M == 1 ? 1 : 6;
-    T2* sstage = buf0 + M * S * N;  // G x UM x LROW
+    T2* sstage = buf1 + M * S * N;  // G x UM x LROW
     // thread-private stash in tensor memory: x (even branch), then e'
     __shared__ uint32_t tmem_slot;
     constexpr int W8 = 8 * (int)sizeof(T2) / 4;
@@ -1073,7 +1126,7 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf_
                         tmem_put8(lane_base, c * W8, v[c]);
                 }
             }
-            fft_rows<T, N, false, M, FiberIdx<N, sizeof(T2)>, SyncGroup, true, Tw<T>[NWR], true>(
+            fft_rows<T, N, false, M, FiberIdx<N, sizeof(T2)>, SyncGroup, true, Tw<T>[NWR], false>(
                 v, buf0, buf1, sidx, tw, t, xc, fsync, wreg);
             const T2* sb = static_cast<const T2*>(sp.data) + sp.branch_base[beta] + off[beta];
             const int64_t bst = sp.block_elems[beta];
@@ -1131,7 +1184,7 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf_
                 if (beta == 0 && p.use_odd)
                     stage(1);  // lands while this branch's inverse transforms run
             }
-            fft_rows<T, N, true, M, FiberIdx<N, sizeof(T2)>, SyncGroup, true, Tw<T>[NWR], true>(
+            fft_rows<T, N, true, M, FiberIdx<N, sizeof(T2)>, SyncGroup, true, Tw<T>[NWR], false>(
                 v, buf0, buf1, sidx, tw, t, xc, fsync, wreg);
         }
         {
@@ -1244,12 +1297,48 @@ static int launch_leaf(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st
     constexpr int S = 4 * G;
     using T2 = typename cx<T>::t;
     const bool ilp = leaf_ilp();
-    const size_t smem = ilp ? 2 * sizeof(T2) * Plan<N>::TW + sizeof(T2) * M * S * N +
+    const size_t smem = ilp ? 2 * sizeof(T2) * Plan<N>::TW + sizeof(T2) * 2 * M * S * N +
                                   sizeof(T2) * G * (M == 1 ? 1 : 6) * (N / 2 + 1)
                             : 2 * sizeof(T2) * Plan<N>::TW + sizeof(T2) * (2 + M) * S * N +
                                   sizeof(T2) * G * (M == 1 ? 1 : 6) * (N / 2 + 1);
     if (smem > 227 * 1024)
         return -1;
+    static const bool phase_dbg = [] {
+        const char* e = getenv("TSK_PHASE_DEBUG");
+        return e && e[0] == '1';
+    }();
+    if (phase_dbg && !ilp) {
+        auto kd = k_leaf<T, N, M, G, true>;
+        int capd = 0;
+        if (int e = prep(kd, smem, N / 8 * S, capd))
+            return e;
+        unsigned long long* dbg = nullptr;
+        cudaMalloc(&dbg, 12 * sizeof(unsigned long long));
+        cudaMemset(dbg, 0, 12 * sizeof(unsigned long long));
+        int64_t units = 1;
+        for (int ax = 0; ax < sp.d - 1; ++ax)
+            units *= (sp.compressed && ax >= sp.d - 3)
+                         ? stored_len(sp.levels[ax], (sp.branch_bits[0] >> ax) & 1u)
+                         : sp.levels[ax];
+        if (!sp.compressed)
+            units = (a.outer + 3) / 4;
+        const int64_t nt = (units + G - 1) / G;
+        kd<<<(unsigned)std::min<int64_t>(nt, capd), N / 8 * S, smem, st>>>(a, sp, dbg);
+        unsigned long long h[12];
+        cudaMemcpy(h, dbg, sizeof h, cudaMemcpyDeviceToHost);
+        cudaFree(dbg);
+        const char* names[12] = {"setup+stage", "x load/stash", "fwd FFT e", "spec wait e", "multiply e",
+                                 "inv FFT e", "odd load", "fwd FFT o", "spec wait o", "multiply o",
+                                 "inv FFT o", "-"};
+        unsigned long long tot = 0;
+        for (int i = 0; i < 12; ++i)
+            tot += h[i];
+        fprintf(stderr, "k_leaf<N=%d,M=%d> phases (thread 0, all CTAs):", N, M);
+        for (int i = 0; i < 11; ++i)
+            fprintf(stderr, " %s %.1f%%", names[i], 100.0 * h[i] / (tot ? tot : 1));
+        fprintf(stderr, "\n");
+        return (int)cudaGetLastError();
+    }
     auto kern = ilp ? k_leaf_ilp<T, N, M, G> : k_leaf<T, N, M, G>;
     int cap = 0;
     if (int e = prep(kern, smem, N / 8 * S, cap))
@@ -1269,7 +1358,7 @@ static int launch_leaf(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st
     }
     const int64_t ntiles = (units + G - 1) / G;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, cap));
-    kern<<<(unsigned)grid, N / 8 * S, smem, st>>>(a, sp);
+    kern<<<(unsigned)grid, N / 8 * S, smem, st>>>(a, sp, nullptr);
     return (int)cudaGetLastError();
 }
 

@@ -1,0 +1,567 @@
+// Leaf-pair pass (K2) with one component per thread and R = N/16..N/8
+// elements per thread: a length-N transform is two in-register stages (radix
+// R, then N/R) and ONE shared-memory exchange among the TF = N/R threads of a
+// (fiber, component) — a half or quarter warp, synchronised with __syncwarp.
+// The m x m spectra multiply couples the components through shared memory once
+// per branch; the even branch's output e' is parked in tensor memory (thread-
+// private lane) while the odd branch runs, and the odd branch re-reads x from
+// L2. A CTA processes one mirror orbit of 4 fibers (compressed spectra rows
+// fetched once, cp.async-staged), m components each.
+//
+// Reference semantics (relative to /root/reference/proj): leaf multiply
+// src/core/kernel.cpp:126-219, leaf FFT/IFFT and deepest merge
+// src/core/engine_split.cpp:67-99, mirror remap kernel.cpp:17-37.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include "tsk_common.cuh"
+#include "tsk_tmem.cuh"
+#include "tsk_wide.cuh"
+
+namespace tsk {
+namespace leaf {
+
+using wide::Dft;
+using wide::Plan;
+using wide::Tw;
+
+__device__ __forceinline__ int orbit_members(int64_t n, int odd, int64_t s, int64_t& partner)
+{
+    const int64_t kp = odd ? n - 1 - s : n - s;
+    partner = kp;
+    if (kp >= 0 && kp < n && kp != s) {
+        bool m;
+        if (mirror_src(n, odd, kp, m) == s && m)
+            return 2;
+    }
+    return 1;
+}
+
+__device__ __forceinline__ void cp_async_bytes8(void* smem, const void* gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_bytes16(void* smem, const void* gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+template <typename T2>
+__device__ __forceinline__ T2 neg_if(T2 v, bool neg)
+{
+    if (neg) {
+        v.x = -v.x;
+        v.y = -v.y;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ Tw<T> twv(typename cx<T>::t w)
+{
+    Tw<T> r;
+    r.lo = w;
+    if constexpr (sizeof(T) == 4)
+        r.hi = mul2(swz(w), make_float2(-1.f, 1.f));
+    else
+        r.hi = make_c<T>(-w.y, w.x);
+    return r;
+}
+
+// v * P_k at k = t + TF m: P_t (register) times exp(-i pi m / R) (constant)
+template <typename T, int R, bool CONJ>
+struct PhaseR {
+    template <int Mi>
+    __device__ __forceinline__ static typename cx<T>::t apply(typename cx<T>::t v, const Tw<T>& pt)
+    {
+        // exp(-+ 2 pi i Mi / (2R)); CONJ flips the sign
+        v = wide::cmul_const<T, 2 * R, Mi, CONJ>(v);
+        return wide::cmul_tw<T, CONJ>(v, pt);
+    }
+};
+
+// Exchange-buffer layout: one pad element per R, so a thread's R-run
+// (t R + q) and the row pattern (t + TF m) are both bank-conflict free and
+// affine in t (addresses are a base register plus immediates).
+template <int N, int R>
+struct Pad {
+    static constexpr int TF = N / R;
+    static constexpr int NP = N + N / R;  // buffer pitch
+    __device__ __forceinline__ static int wr(int t, int q) { return t * (R + 1) + q; }
+    __device__ __forceinline__ static int rd(int t, int m) { return t + TF * m + (TF * m) / R; }
+};
+
+// s with both parts' sign bits flipped when neg (integer pipe, not FMA)
+template <typename T>
+__device__ __forceinline__ typename cx<T>::t flip_bits(typename cx<T>::t s, uint32_t neg)
+{
+    if constexpr (sizeof(T) == 4) {
+        const uint32_t b = neg << 31;
+        return make_float2(__uint_as_float(__float_as_uint(s.x) ^ b),
+                           __uint_as_float(__float_as_uint(s.y) ^ b));
+    } else {
+        const long long b = (long long)neg << 63;
+        return make_double2(__longlong_as_double(__double_as_longlong(s.x) ^ b),
+                            __longlong_as_double(__double_as_longlong(s.y) ^ b));
+    }
+}
+
+// acc (+)= x * s; packed f32x2: x s = s.x x + s.y (i x)
+template <typename T>
+__device__ __forceinline__ typename cx<T>::t cmac(typename cx<T>::t acc, typename cx<T>::t x,
+                                                  typename cx<T>::t s, bool first)
+{
+    if constexpr (sizeof(T) == 4) {
+        const float2 ix = mul2(swz(x), make_float2(-1.f, 1.f));
+        const float2 a = first ? mul2(bc_x(s), x) : fma2(bc_x(s), x, acc);
+        return fma2(bc_y(s), ix, a);
+    } else {
+        const typename cx<T>::t pr = cmul(x, s);
+        return first ? pr : cadd(acc, pr);
+    }
+}
+
+// a + e * scale
+template <typename T>
+__device__ __forceinline__ typename cx<T>::t fma_s(typename cx<T>::t e, T scale, typename cx<T>::t a)
+{
+    if constexpr (sizeof(T) == 4)
+        return fma2(e, make_float2(scale, scale), a);
+    else
+        return make_c<T>(e.x * scale + a.x, e.y * scale + a.y);
+}
+
+// acc (+)= sgn * x * s; packed f32x2: x s = x.x s + x.y (i s)
+template <typename T>
+__device__ __forceinline__ typename cx<T>::t cmac_sgn(typename cx<T>::t acc, typename cx<T>::t x,
+                                                      typename cx<T>::t s, T sgn, bool first)
+{
+    if constexpr (sizeof(T) == 4) {
+        const float2 ss = mul2(s, make_float2(sgn, sgn));
+        const float2 rs = mul2(swz(s), make_float2(-sgn, sgn));
+        const float2 a = first ? mul2(bc_x(x), ss) : fma2(bc_x(x), ss, acc);
+        return fma2(bc_y(x), rs, a);
+    } else {
+        const typename cx<T>::t ss = make_c<T>(s.x * sgn, s.y * sgn);
+        const typename cx<T>::t pr = cmul(x, ss);
+        return first ? pr : cadd(acc, pr);
+    }
+}
+
+template <int B, int E, class F>
+__device__ __forceinline__ void sfor(F&& f)
+{
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        sfor<B + 1, E>(f);
+    }
+}
+
+// One length-N transform of this thread's row pattern v[m] = x[t + TF m].
+template <typename T, int N, int R, bool INV>
+__device__ __forceinline__ void fft_one(typename cx<T>::t (&v)[R], typename cx<T>::t* buf,
+                                        const typename cx<T>::t* tw, int t)
+{
+    using T2 = typename cx<T>::t;
+    constexpr int TF = N / R;
+    constexpr int P2 = N / R;
+    constexpr int G2 = R / P2;
+    static_assert(P2 <= R, "two-stage plan needs N <= R^2");
+    // stage A: radix R, butterfly j = t (Ns = 1) -> positions t*R + q
+    Dft<T, R, INV>::run(v);
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+        buf[Pad<N, R>::wr(t, q)] = v[q];
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < R; ++m)
+        v[m] = buf[Pad<N, R>::rd(t, m)];
+    __syncwarp();
+    // stage B: radix P2, Ns = R, butterflies j = t + i TF (i < G2), twiddle w_N^{r j}
+#pragma unroll
+    for (int i = 0; i < G2; ++i) {
+        const int j = t + i * TF;
+        T2 a[P2];
+        a[0] = v[i];
+#pragma unroll
+        for (int r = 1; r < P2; ++r) {
+            const Tw<T> w = wide::load_tw<T>(tw + j * (P2 - 1) + (r - 1));
+            a[r] = wide::cmul_tw<T, INV>(v[i + r * G2], w);
+        }
+        Dft<T, P2, INV>::run(a);
+#pragma unroll
+        for (int q = 0; q < P2; ++q)
+            v[i + q * G2] = a[q];
+        asm volatile("" ::: "memory");  // bound the twiddle loads in flight
+    }
+}
+
+// units (orbits) per CTA: warps per CTA a multiple of 4 (even split over the
+// SM sub-partitions' register files)
+constexpr int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }
+template <int N, int R, int M>
+constexpr int leaf1_g()
+{
+    return 128 / gcd_i(128, 4 * M * (N / R));
+}
+
+template <typename T, int N, int R, int M, int G = leaf1_g<N, R, M>()>
+__global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 * M * (N / R) < 384 ? 384 / (G * 4 * M * (N / R)) : 1) k_leaf1(tsk_axis p, tsk_spectra sp)
+{
+    using T2 = typename cx<T>::t;
+    constexpr int TF = N / R;
+    constexpr int P2 = N / R;
+    constexpr int CF = 4 * M;  // (fiber, component) groups per CTA
+    constexpr int UT = CF * TF;  // threads per unit
+    constexpr int NT = G * UT;
+    constexpr int NP = Pad<N, R>::NP;
+    constexpr int LROW = N / 2 + 1;
+    constexpr int UM = M == 1 ? 1 : 6;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T2* tw = reinterpret_cast<T2*>(smem_raw);         // R x (P2 - 1) stage-B twiddles
+    T2* bufs = tw + R * (P2 - 1);                      // G x CF x NP exchange / mix buffers
+    T2* stg0 = bufs + G * CF * NP;                     // G x UM x LROW staged spectra rows
+    __shared__ uint32_t tmem_slot;
+
+    for (int e = threadIdx.x; e < R * (P2 - 1); e += NT) {
+        const int j = e / (P2 - 1), r = e % (P2 - 1) + 1;
+        tw[e] = ldg_c(static_cast<const T2*>(p.roots) + (r * j) % N);
+    }
+
+    // thread layout [component][unit][fiber][t]: the component is warp-uniform
+    // (the spectra multiply is specialised per component, no divergence)
+    const int c = threadIdx.x / (G * 4 * TF);
+    const int fs = (threadIdx.x / TF) % (G * 4);
+    const int gi = fs / 4, f = fs % 4;
+    const int t = threadIdx.x % TF;
+    const int lt = (c * 4 + f) * TF + t;  // index among this unit's threads
+    const int cf = f * M + c;
+    T2* buf = bufs + (gi * CF + cf) * NP;
+    T2* fbufs = bufs + gi * CF * NP;  // this unit's component buffers
+    T2* stg = stg0 + gi * UM * LROW;
+    const Tw<T> pt = twv<T>(ldg_c(static_cast<const T2*>(p.phase) + t));
+    // output scale 1/(2n) folded into the odd branch's conj phase and the
+    // merge FMA (the spectra multiply only flips signs)
+    const T scale = (T)p.scale;
+    const Tw<T> pts = twv<T>(make_c<T>(pt.lo.x * scale, pt.lo.y * scale));
+
+    // e' parked in TMEM when it is a multiple of 32 words, else in registers
+    constexpr int EW = R * (int)sizeof(T2) / 4;
+    constexpr bool TM = EW % 32 == 0;
+    constexpr int NW = NT / 32 > 0 ? NT / 32 : 1;
+    constexpr int TCOLS = tmem_cols_pow2(EW * ((NW + 3) / 4));
+    uint32_t tbase = 0, lane_base = 0;
+    if constexpr (TM) {
+        tbase = tmem_alloc(&tmem_slot, TCOLS);
+        lane_base = tbase + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16) +
+                    (uint32_t)(EW * ((threadIdx.x / 32) / 4));
+    } else {
+        __syncthreads();
+    }
+
+    const int d = sp.d;
+    const int U = sp.n_unique;
+    const bool ue = p.use_even, uo = p.use_odd, both = ue && uo;
+    const uint32_t bits = sp.branch_bits[0];
+    uint32_t lastneg = 0;
+    for (int uu = 0; uu < U; ++uu)
+        lastneg |= ((sp.skew_mask[uu] >> (d - 1)) & 1u) << uu;
+    // orbit axes: the last two outer axes (A1, A2); unit = (rest, s1, s2)
+    const int A2 = d - 2, A1 = d - 3;
+    int64_t n1 = 1, n2 = 1, st1 = 1, st2 = 1;
+    if (A2 >= 0) {
+        n2 = sp.levels[A2];
+        st2 = stored_len(n2, (bits >> A2) & 1u);
+    }
+    if (A1 >= 0) {
+        n1 = sp.levels[A1];
+        st1 = stored_len(n1, (bits >> A1) & 1u);
+    }
+    int64_t rest = 1;
+    for (int a = 0; a < A1; ++a)
+        rest *= sp.levels[a];
+    const int64_t units = rest * st1 * st2;
+    const T2* src = static_cast<const T2*>(p.src0);
+    T2* dst = static_cast<T2*>(p.dst0);
+    const T2* spec = static_cast<const T2*>(sp.data);
+    T2 ekeep[TM ? 1 : R];
+
+    for (int64_t tile = blockIdx.x; tile * G < units; tile += gridDim.x) {
+        int64_t u = tile * G + gi;
+        const bool uvalid = u < units;
+        if (!uvalid)
+            u = units - 1;  // runs in lockstep (barriers), stores nothing
+        // ---- unit geometry: fiber g of orbit member f, spectra row, signs.
+        // Members past the orbit size alias a real member (loads stay in
+        // range) and skip the store.
+        bool valid;
+        int64_t g, off0, off1;
+        uint32_t neg = 0;
+        {
+            const uint32_t u32 = (uint32_t)u, st2u = (uint32_t)st2, st1u = (uint32_t)st1;
+            const uint32_t q2 = u32 / st2u, q1 = q2 / st1u;
+            const int64_t s2 = u32 - q2 * st2u, s1 = q2 - q1 * st1u, r = q1;
+            int64_t p1 = 0, p2 = 0;
+            const int c1 = A1 >= 0 ? orbit_members(n1, (bits >> A1) & 1u, s1, p1) : 1;
+            const int c2 = A2 >= 0 ? orbit_members(n2, (bits >> A2) & 1u, s2, p2) : 1;
+            valid = uvalid && f < c1 * c2;
+            const int i1 = (f % (c1 * c2)) / c2, i2 = f % c2;
+            const int64_t kk1 = A1 < 0 ? 0 : (i1 ? p1 : s1);
+            const int64_t kk2 = A2 < 0 ? 0 : (i2 ? p2 : s2);
+            for (int uu = 0; uu < U; ++uu) {
+                if (A1 >= 0 && i1)
+                    neg ^= ((sp.skew_mask[uu] >> A1) & 1u) << uu;
+                if (A2 >= 0 && i2)
+                    neg ^= ((sp.skew_mask[uu] >> A2) & 1u) << uu;
+            }
+            int64_t rsrc = 0, rstr = 1, gr = r, rfull = 0, rmul = 1;
+            for (int a = A1 - 1; a >= 0; --a) {
+                const int64_t na = sp.levels[a];
+                const int64_t ka = gr % na;
+                gr /= na;
+                const int odd = (bits >> a) & 1u;
+                bool mm;
+                rsrc += mirror_src(na, odd, ka, mm) * rstr;
+                rstr *= stored_len(na, odd);
+                rfull += ka * rmul;
+                rmul *= na;
+                if (mm)
+                    for (int uu = 0; uu < U; ++uu)
+                        neg ^= ((sp.skew_mask[uu] >> a) & 1u) << uu;
+            }
+            g = (rfull * n1 + kk1) * n2 + kk2;
+            const int64_t row = (rsrc * st1 + s1) * st2 + s2;
+            off0 = row * (N / 2 + 1);
+            off1 = row * (N / 2);
+        }
+        // sign masks per unique component: bit uu of neg (unmirrored k) and
+        // of neg ^ lastneg (mirrored k)
+        const uint32_t neg0 = neg, neg1 = neg ^ lastneg;
+        auto stage_row = [&](int beta) {
+            const int L = beta ? N / 2 : N / 2 + 1;
+            const T2* rowp = spec + sp.branch_base[beta] + (beta ? off1 : off0);
+            for (int e = lt; e < UM * L; e += UT) {
+                const int uu = e / L, kk = e - uu * L;
+                if constexpr (sizeof(T2) == 8)
+                    cp_async_bytes8(stg + uu * LROW + kk, rowp + uu * sp.block_elems[beta] + kk);
+                else
+                    cp_async_bytes16(stg + uu * LROW + kk, rowp + uu * sp.block_elems[beta] + kk);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        stage_row(ue ? 0 : 1);
+        const T2* xin = src + c * p.cstride + g * N + t;
+
+#pragma unroll
+        for (int beta = 0; beta < 2; ++beta) {
+            if (beta == 0 ? !ue : !uo)
+                continue;
+            T2 v[R];
+#pragma unroll
+            for (int m = 0; m < R; ++m)
+                v[m] = xin[m * TF];
+            if (beta == 1)
+                sfor<0, R>([&](auto I) {
+                    constexpr int mi = decltype(I)::value;
+                    v[mi] = PhaseR<T, R, false>::template apply<mi>(v[mi], pt);
+                });
+            fft_one<T, N, R, false>(v, buf, tw, t);
+
+            // ---- spectra multiply y_c = sum_c' T_{c c'} x_c' (components meet in smem)
+            if (M > 1) {
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    buf[Pad<N, R>::rd(t, m)] = v[m];
+            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+            // stored half-spectrum index: k = t + TF m below N/2, mirrored
+            // (N - beta - k) from N/2 up; k = N/2 (t = 0, even) maps to itself
+            auto mix = [&](auto CI) {
+                constexpr int C = decltype(CI)::value;
+                const T2* sA = stg + t;
+                const T2* sB = stg + (N - beta - t);
+                const bool t0 = t == 0;
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    const bool mirm = 2 * m >= R;
+                    const T2* sp_ = mirm ? sB - TF * m : sA + TF * m;
+                    T2 acc;
+                    sfor<0, M>([&](auto CC) {
+                        constexpr int cc = decltype(CC)::value;
+                        constexpr int lo = C < cc ? C : cc, hi = C < cc ? cc : C;
+                        constexpr int uu = M == 1 ? 0 : 3 * lo - (lo * (lo - 1)) / 2 + (hi - lo);
+                        // sign: unmirrored neg0, mirrored neg1 (k = N/2 at t = 0 unmirrored)
+                        uint32_t ng;
+                        if (!mirm)
+                            ng = neg0;
+                        else if (beta == 0 && 2 * m == R)
+                            ng = t0 ? neg0 : neg1;
+                        else
+                            ng = neg1;
+                        const T2 s_ = flip_bits<T>(sp_[uu * LROW], (ng >> uu) & 1u);
+                        const T2 xv = cc == C ? v[m] : fbufs[(f * M + cc) * NP + Pad<N, R>::rd(t, m)];
+                        acc = cmac<T>(acc, xv, s_, cc == 0);
+                    });
+                    v[m] = acc;
+                    if (m % 2 == 1)
+                        asm volatile("" ::: "memory");  // bound the loads in flight
+                }
+            };
+            if constexpr (M == 1) {
+                mix(std::integral_constant<int, 0>{});
+            } else {
+                if (c == 0)
+                    mix(std::integral_constant<int, 0>{});
+                else if (c == 1)
+                    mix(std::integral_constant<int, 1>{});
+                else
+                    mix(std::integral_constant<int, 2>{});
+            }
+            __syncthreads();  // staged row and mix buffers free
+            if (beta == 0 && uo)
+                stage_row(1);
+            fft_one<T, N, R, true>(v, buf, tw, t);
+
+            if (beta == 0 && both) {
+                if constexpr (TM)
+                    tmem_park<T, R>(lane_base, v);
+                else
+#pragma unroll
+                    for (int m = 0; m < R; ++m)
+                        ekeep[m] = v[m];
+            } else {
+                // e' comes back from TMEM 32 words at a time (bounded registers)
+                constexpr int EPC = TM ? 32 / ((int)sizeof(T2) / 4) : R;
+                T2* yout = dst + c * p.cstride + g * N + t;
+                sfor<0, R / EPC>([&](auto C) {
+                    constexpr int c0 = decltype(C)::value * EPC;
+                    T2 e[EPC];
+                    if (both) {
+                        if constexpr (TM) {
+                            uint32_t r[32];
+                            tmem_ld32(lane_base + c0 * ((int)sizeof(T2) / 4), r);
+#pragma unroll
+                            for (int i = 0; i < EPC; ++i)
+                                e[i] = Words<T2>::make(r + i * Words<T2>::W);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < EPC; ++i)
+                                e[i] = ekeep[c0 + i];
+                        }
+                    }
+                    sfor<0, EPC>([&](auto I) {
+                        constexpr int mi = c0 + decltype(I)::value;
+                        T2 a;
+                        if (beta == 1) {
+                            a = PhaseR<T, R, true>::template apply<mi>(v[mi], pts);
+                            if (both)
+                                a = fma_s<T>(e[decltype(I)::value], scale, a);
+                        } else {
+                            a = make_c<T>(v[mi].x * scale, v[mi].y * scale);
+                        }
+                        if (valid)
+                            yout[mi * TF] = a;
+                    });
+                });
+            }
+        }
+    }
+    if constexpr (TM)
+        tmem_free(tbase, TCOLS);
+}
+
+static int sm_count()
+{
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 148;
+}
+
+template <typename T, int N, int R, int M>
+static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
+{
+    using T2 = typename cx<T>::t;
+    constexpr int TF = N / R;
+    constexpr int NP = Pad<N, R>::NP;
+    constexpr int G = leaf1_g<N, R, M>();
+    constexpr int NT = G * 4 * M * TF;
+    const size_t smem =
+        sizeof(T2) * (R * (N / R - 1) + G * 4 * M * NP + G * (M == 1 ? 1 : 6) * (N / 2 + 1));
+    if (smem > 227 * 1024)
+        return -1;
+    auto kern = k_leaf1<T, N, R, M>;
+    static thread_local int cached_dev = -1, cap = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != cached_dev) {
+        if (int e = (int)cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem))
+            return e;
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+        // TMEM: every resident CTA allocates its columns
+        constexpr int EW = R * (int)sizeof(T2) / 4;
+        constexpr int NW = NT / 32 > 0 ? NT / 32 : 1;
+        constexpr int TC = tmem_cols_pow2(EW * ((NW + 3) / 4));
+        if (EW % 32 == 0 && per_sm * TC > 512)
+            per_sm = 512 / TC;
+        if (getenv("TSK_DEBUG_OCC"))
+            fprintf(stderr, "k_leaf1<%d,%d,%d,%d>: %d CTAs/SM, %zu B smem, %d threads\n",
+                    (int)sizeof(T), N, R, M, per_sm, smem, NT);
+        cap = sm_count() * (per_sm > 0 ? per_sm : 1);
+        cached_dev = dev;
+    }
+    int64_t units = 1;
+    for (int ax = 0; ax < sp.d - 1; ++ax)
+        units *= ax >= sp.d - 3 ? stored_len(sp.levels[ax], (sp.branch_bits[0] >> ax) & 1u)
+                                : sp.levels[ax];
+    const int64_t tiles = (units + G - 1) / G;
+    const int64_t grid = tiles < cap ? tiles : cap;
+    kern<<<(unsigned)(grid > 0 ? grid : 1), NT, smem, st>>>(a, sp);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, int M>
+static int dispatch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
+{
+    switch (a.n) {
+    case 64: return launch<T, 64, 8, M>(a, sp, st);
+    case 128: return launch<T, 128, 16, M>(a, sp, st);
+    case 256: return launch<T, 256, 16, M>(a, sp, st);
+    case 512:  // complex128 at R = 32 spills; the 8-point kernel handles it
+        return sizeof(T) == 4 ? launch<T, 512, 32, M>(a, sp, st) : -1;
+    default: return -1;
+    }
+}
+
+}  // namespace leaf
+}  // namespace tsk
+
+// -1: not covered (caller falls back), else the launch cudaError_t.
+extern "C" int tsk_leaf1_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream)
+{
+    if (a->inner != 1 || !sp->compressed)
+        return -1;
+    static const int8_t canon[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+    auto st = (cudaStream_t)stream;
+    if (sp->m == 1)
+        return a->prec ? tsk::leaf::dispatch<float, 1>(*a, *sp, st)
+                       : tsk::leaf::dispatch<double, 1>(*a, *sp, st);
+    if (sp->m == 3 && sp->n_unique == 6) {
+        for (int i = 0; i < 9; ++i)
+            if (sp->comp_map[i] != canon[i])
+                return -1;
+        return a->prec ? tsk::leaf::dispatch<float, 3>(*a, *sp, st)
+                       : tsk::leaf::dispatch<double, 3>(*a, *sp, st);
+    }
+    return -1;
+}

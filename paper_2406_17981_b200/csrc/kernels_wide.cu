@@ -26,214 +26,10 @@
 
 #include "tsk_common.cuh"
 #include "tsk_tmem.cuh"
+#include "tsk_wide.cuh"
 
 namespace tsk {
 namespace wide {
-
-constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
-
-// cos(2 pi k / 64), k = 0..16 (quarter wave; the rest by symmetry)
-__host__ __device__ constexpr double cos64q(int k)
-{
-    constexpr double t[17] = {1.0,
-                              0.99518472667219688624,
-                              0.98078528040323044913,
-                              0.95694033573220886494,
-                              0.92387953251128675613,
-                              0.88192126434835502971,
-                              0.83146961230254523708,
-                              0.77301045336273696081,
-                              0.70710678118654752440,
-                              0.63439328416364549822,
-                              0.55557023301960222474,
-                              0.47139673682599764856,
-                              0.38268343236508977173,
-                              0.29028467725446236764,
-                              0.19509032201612826785,
-                              0.09801714032956060199,
-                              0.0};
-    return t[k];
-}
-__host__ __device__ constexpr double cos64(int k)
-{
-    k = ((k % 64) + 64) % 64;
-    if (k <= 16)
-        return cos64q(k);
-    if (k <= 32)
-        return -cos64q(32 - k);
-    if (k <= 48)
-        return -cos64q(k - 32);
-    return cos64q(64 - k);
-}
-__host__ __device__ constexpr double sin64(int k) { return cos64(k - 16); }
-
-// v * exp(sgn 2 pi i k / P) for a compile-time angle (P | 64).
-template <typename T, int P, int K, bool INV>
-__device__ __forceinline__ typename cx<T>::t cmul_const(typename cx<T>::t v)
-{
-    constexpr int k64 = ((K % P) + P) % P * (64 / P);
-    constexpr double c = cos64(k64);
-    constexpr double s = (INV ? 1.0 : -1.0) * sin64(k64);
-    if constexpr (k64 == 0) {
-        return v;
-    } else if constexpr (k64 == 32) {
-        return make_c<T>(-v.x, -v.y);
-    } else if constexpr (k64 == 16 || k64 == 48) {
-        // multiply by +-i
-        if constexpr (sizeof(T) == 4)
-            return mul2(swz(v), s > 0 ? make_float2(-1.f, 1.f) : make_float2(1.f, -1.f));
-        else
-            return s > 0 ? make_c<T>(-v.y, v.x) : make_c<T>(v.y, -v.x);
-    } else {
-        if constexpr (sizeof(T) == 4)
-            return fma2(bc_y(v), make_float2((float)-s, (float)c),
-                        mul2(bc_x(v), make_float2((float)c, (float)s)));
-        else
-            return make_c<T>(v.x * c - v.y * s, v.x * s + v.y * c);
-    }
-}
-
-// In-register DFT of size P on a[0..P), natural order in and out.
-template <typename T, int P, bool INV>
-struct Dft {
-    using T2 = typename cx<T>::t;
-    // split P = P1 * P2: input r = P2 a + b, output q = c + P1 e
-    static constexpr int P1 = P >= 16 ? 4 : 2;
-    static constexpr int P2 = P / P1;
-    template <int B, int C>
-    __device__ __forceinline__ static void tw(T2* a)
-    {
-        a[P2 * C + B] = cmul_const<T, P, B * C, INV>(a[P2 * C + B]);
-    }
-    __device__ __forceinline__ static void run(T2* a)
-    {
-        if constexpr (P == 1) {
-        } else if constexpr (P == 2) {
-            const T2 x = a[0], y = a[1];
-            a[0] = cadd(x, y);
-            a[1] = csub(x, y);
-        } else if constexpr (P == 4) {
-            dft4<T, INV>(a[0], a[1], a[2], a[3]);
-        } else if constexpr (P == 8) {
-            dft_small<T, 8, INV>(a, nullptr, 0);
-        } else {
-            // step 1: P2 transforms of length P1 on stride-P2 subsequences
-#pragma unroll
-            for (int b = 0; b < P2; ++b) {
-                T2 s[P1];
-#pragma unroll
-                for (int i = 0; i < P1; ++i)
-                    s[i] = a[P2 * i + b];
-                Dft<T, P1, INV>::run(s);
-#pragma unroll
-                for (int i = 0; i < P1; ++i)
-                    a[P2 * i + b] = s[i];
-            }
-            // twiddles w_P^{b c}
-            twiddles(a, std::make_integer_sequence<int, P1 * P2>{});
-            // step 2: P1 transforms of length P2 on contiguous groups
-            T2 o[P];
-#pragma unroll
-            for (int c = 0; c < P1; ++c) {
-                T2 s[P2];
-#pragma unroll
-                for (int i = 0; i < P2; ++i)
-                    s[i] = a[P2 * c + i];
-                Dft<T, P2, INV>::run(s);
-#pragma unroll
-                for (int e = 0; e < P2; ++e)
-                    o[c + P1 * e] = s[e];
-            }
-#pragma unroll
-            for (int q = 0; q < P; ++q)
-                a[q] = o[q];
-        }
-    }
-    template <int... Is>
-    __device__ __forceinline__ static void twiddles(T2* a, std::integer_sequence<int, Is...>)
-    {
-        (tw<Is % P2, Is / P2>(a), ...);
-    }
-};
-
-template <int N, int R>
-struct Plan {
-    static constexpr int TF = N / R;
-    static constexpr int L = ilog2(N), LR = ilog2(R);
-    static constexpr int NST = (L + LR - 1) / LR;
-    static constexpr int radix(int s)
-    {
-        return s < NST - 1 ? R : (1 << (L - LR * (NST - 1)));
-    }
-    static constexpr int ns(int s)
-    {
-        int v = 1;
-        for (int i = 0; i < s; ++i)
-            v *= radix(i);
-        return v;
-    }
-    static constexpr int tw_off(int s)
-    {
-        int o = 0;
-        for (int i = 1; i < s; ++i)
-            o += ns(i) * (radix(i) - 1);
-        return o;
-    }
-    static constexpr int TW = tw_off(NST) > 0 ? tw_off(NST) : 1;
-};
-
-template <typename T>
-struct tw4;
-template <>
-struct tw4<float> {
-    using t = float4;
-};
-template <>
-struct tw4<double> {
-    using t = double4;
-};
-
-template <typename T>
-struct Tw {
-    typename cx<T>::t lo, hi;
-};
-
-// Tables keep only w (64-bit reads: 2 wavefronts per warp even when
-// broadcast, a 128-bit read costs 4); rot(w) = (-w.y, w.x) is one FMUL2.
-template <typename T>
-__device__ __forceinline__ Tw<T> load_tw(const typename cx<T>::t* p)
-{
-    Tw<T> w;
-    w.lo = *p;
-    if constexpr (sizeof(T) == 4)
-        w.hi = mul2(swz(w.lo), make_float2(-1.f, 1.f));
-    else
-        w.hi = make_c<T>(-w.lo.y, w.lo.x);
-    return w;
-}
-
-template <typename T>
-__device__ __forceinline__ typename tw4<T>::t make_tw(typename cx<T>::t w)
-{
-    typename tw4<T>::t r;
-    r.x = w.x;
-    r.y = w.y;
-    r.z = -w.y;
-    r.w = w.x;
-    return r;
-}
-
-template <typename T, bool CONJ>
-__device__ __forceinline__ typename cx<T>::t cmul_tw(typename cx<T>::t v, const Tw<T>& w)
-{
-    if constexpr (sizeof(T) == 4) {
-        if (CONJ)
-            return fma2(bc_y(v), swz(w.lo), mul2(bc_x(v), swz(w.hi)));
-        return fma2(bc_y(v), w.hi, mul2(bc_x(v), w.lo));
-    } else {
-        return CONJ ? cmulc(v, w.lo) : cmul(v, w.lo);
-    }
-}
 
 template <typename T, int N, int R>
 __device__ void fill_tables(typename cx<T>::t* tw, typename cx<T>::t* ph,

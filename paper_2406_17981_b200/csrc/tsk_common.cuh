@@ -171,29 +171,31 @@ __device__ __forceinline__ void dft4(typename cx<T>::t& x0, typename cx<T>::t& x
     x3 = csub(d0, d1);
 }
 
-// Packed complex64 radix-4: -i d1 folded into one FFMA2 with a (+-1, -+1)
-// lane-sign pair on the swapped operand.
+// +-i a as a lane swap with one lane negated: ptxas folds it into the
+// consuming FADD2/FFMA2 operand (.LO_HI.NP), so it costs no instruction.
+__device__ __forceinline__ float2 mul_i(float2 a) { return make_float2(-a.y, a.x); }
+__device__ __forceinline__ float2 mul_negi(float2 a) { return make_float2(a.y, -a.x); }
+
+// Packed complex64 radix-4: 8 FADD2, the -+i folded into operands.
 template <>
 __device__ __forceinline__ void dft4<float, false>(float2& x0, float2& x1, float2& x2, float2& x3)
 {
-    const float2 pm = make_float2(1.f, -1.f), mp = make_float2(-1.f, 1.f);
     const float2 s0 = add2(x0, x2), d0 = sub2(x0, x2);
     const float2 s1 = add2(x1, x3), d1 = sub2(x1, x3);
     x0 = add2(s0, s1);
     x2 = sub2(s0, s1);
-    x1 = fma2(swz(d1), pm, d0);  // d0 - i d1
-    x3 = fma2(swz(d1), mp, d0);  // d0 + i d1
+    x1 = add2(d0, mul_negi(d1));  // d0 - i d1
+    x3 = add2(d0, mul_i(d1));     // d0 + i d1
 }
 template <>
 __device__ __forceinline__ void dft4<float, true>(float2& x0, float2& x1, float2& x2, float2& x3)
 {
-    const float2 pm = make_float2(1.f, -1.f), mp = make_float2(-1.f, 1.f);
     const float2 s0 = add2(x0, x2), d0 = sub2(x0, x2);
     const float2 s1 = add2(x1, x3), d1 = sub2(x1, x3);
     x0 = add2(s0, s1);
     x2 = sub2(s0, s1);
-    x1 = fma2(swz(d1), mp, d0);  // d0 + i d1
-    x3 = fma2(swz(d1), pm, d0);  // d0 - i d1
+    x1 = add2(d0, mul_i(d1));     // d0 + i d1
+    x3 = add2(d0, mul_negi(d1));  // d0 - i d1
 }
 
 // Packed complex64 radix-8 (DIT from two radix-4): 28 FP instructions.
@@ -204,18 +206,18 @@ __device__ __forceinline__ void dft8_packed(float2* v)
     float2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
     dft4<float, INV>(e0, e1, e2, e3);
     dft4<float, INV>(o0, o1, o2, o3);
+    // twiddles with broadcast immediates: w8 = h (1 - i), w8^3 = -h (1 + i)
     const float h = 0.70710678118654752440f;
-    const float2 pm = make_float2(1.f, -1.f), mp = make_float2(-1.f, 1.f);
     if (!INV) {
-        o1 = fma2(bc_y(o1), make_float2(h, h), mul2(bc_x(o1), make_float2(h, -h)));     // * w8
-        o3 = fma2(bc_y(o3), make_float2(h, -h), mul2(bc_x(o3), make_float2(-h, -h)));   // * w8^3
-        v[2] = fma2(swz(o2), pm, e2);
-        v[6] = fma2(swz(o2), mp, e2);
+        o1 = mul2(add2(o1, mul_negi(o1)), make_float2(h, h));
+        o3 = mul2(add2(o3, mul_i(o3)), make_float2(-h, -h));
+        v[2] = add2(e2, mul_negi(o2));
+        v[6] = add2(e2, mul_i(o2));
     } else {
-        o1 = fma2(bc_y(o1), make_float2(-h, h), mul2(bc_x(o1), make_float2(h, h)));
-        o3 = fma2(bc_y(o3), make_float2(-h, -h), mul2(bc_x(o3), make_float2(-h, h)));
-        v[2] = fma2(swz(o2), mp, e2);
-        v[6] = fma2(swz(o2), pm, e2);
+        o1 = mul2(add2(o1, mul_i(o1)), make_float2(h, h));
+        o3 = mul2(add2(o3, mul_negi(o3)), make_float2(-h, -h));
+        v[2] = add2(e2, mul_i(o2));
+        v[6] = add2(e2, mul_negi(o2));
     }
     v[0] = add2(e0, o0);
     v[4] = sub2(e0, o0);

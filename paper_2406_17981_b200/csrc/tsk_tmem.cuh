@@ -11,6 +11,37 @@
 
 namespace tsk {
 
+// 32-bit words of a complex value, by member access (a reinterpret_cast of a
+// register array's address would force the array into local memory)
+template <typename T2>
+struct Words;
+template <>
+struct Words<float2> {
+    static constexpr int W = 2;
+    __device__ __forceinline__ static uint32_t get(const float2& v, int j)
+    {
+        return __float_as_uint(j == 0 ? v.x : v.y);
+    }
+    __device__ __forceinline__ static float2 make(const uint32_t* r)
+    {
+        return make_float2(__uint_as_float(r[0]), __uint_as_float(r[1]));
+    }
+};
+template <>
+struct Words<double2> {
+    static constexpr int W = 4;
+    __device__ __forceinline__ static uint32_t get(const double2& v, int j)
+    {
+        const double d = j < 2 ? v.x : v.y;
+        return (uint32_t)((j & 1) ? __double2hiint(d) : __double2loint(d));
+    }
+    __device__ __forceinline__ static double2 make(const uint32_t* r)
+    {
+        return make_double2(__hiloint2double((int)r[1], (int)r[0]),
+                            __hiloint2double((int)r[3], (int)r[2]));
+    }
+};
+
 
 __device__ __forceinline__ uint32_t tmem_alloc(uint32_t* slot, int cols)
 {
@@ -80,7 +111,8 @@ __device__ __forceinline__ void tmem_park(uint32_t lane_base, const typename cx<
         uint32_t r[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-            r[i] = reinterpret_cast<const uint32_t*>(&v[0])[c * 32 + i];
+            r[i] = Words<typename cx<T>::t>::get(v[(c * 32 + i) / Words<typename cx<T>::t>::W],
+                                                 (c * 32 + i) % Words<typename cx<T>::t>::W);
         tmem_st32(lane_base + c * 32, r);
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -95,8 +127,8 @@ __device__ __forceinline__ void tmem_restore(uint32_t lane_base, typename cx<T>:
         uint32_t r[32];
         tmem_ld32(lane_base + c * 32, r);
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-            reinterpret_cast<uint32_t*>(&v[0])[c * 32 + i] = r[i];
+        for (int i = 0; i < 32; i += Words<typename cx<T>::t>::W)
+            v[(c * 32 + i) / Words<typename cx<T>::t>::W] = Words<typename cx<T>::t>::make(r + i);
     }
 }
 
@@ -137,7 +169,7 @@ __device__ __forceinline__ void tmem_put8(uint32_t lane_base, int col, const T2 
         uint32_t r[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-            r[i] = reinterpret_cast<const uint32_t*>(&v[0])[c * 16 + i];
+            r[i] = Words<T2>::get(v[(c * 16 + i) / Words<T2>::W], (c * 16 + i) % Words<T2>::W);
         tmem_st16(lane_base + col + c * 16, r);
     }
 }
@@ -152,8 +184,8 @@ __device__ __forceinline__ void tmem_get8(uint32_t lane_base, int col, T2 (&v)[8
         tmem_ld16(lane_base + col + c * 16, r);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-            reinterpret_cast<uint32_t*>(&v[0])[c * 16 + i] = r[i];
+        for (int i = 0; i < 16; i += Words<T2>::W)
+            v[(c * 16 + i) / Words<T2>::W] = Words<T2>::make(r + i);
     }
 }
 
