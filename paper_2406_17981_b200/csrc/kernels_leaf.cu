@@ -244,6 +244,9 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     T2* buf = bufs + (gi * CF + cf) * NP;
     T2* fbufs = bufs + gi * CF * NP;  // this unit's component buffers
     T2* stg = stg0 + gi * UM * LROW;
+    // each unit (6 warps for m = 3) synchronises on its own named barrier, so
+    // the units of a CTA drift apart and overlap memory with arithmetic
+    auto unit_sync = [gi]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + gi), "n"(UT) : "memory"); };
     const Tw<T> pt = twv<T>(ldg_c(static_cast<const T2*>(p.phase) + t));
     // output scale 1/(2n) folded into the odd branch's conj phase and the
     // merge FMA (the spectra multiply only flips signs)
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                     buf[Pad<N, R>::rd(t, m)] = v[m];
             }
             asm volatile("cp.async.wait_group 0;" ::: "memory");
-            __syncthreads();
+            unit_sync();
             // stored half-spectrum index: k = t + TF m below N/2, mirrored
             // (N - beta - k) from N/2 up; k = N/2 (t = 0, even) maps to itself
             auto mix = [&](auto CI) {
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 else
                     mix(std::integral_constant<int, 2>{});
             }
-            __syncthreads();  // staged row and mix buffers free
+            unit_sync();  // staged row and mix buffers free
             if (beta == 0 && uo)
                 stage_row(1);
             fft_one<T, N, R, true>(v, buf, tw, t);
