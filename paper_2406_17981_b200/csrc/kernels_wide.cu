@@ -22,6 +22,8 @@
 // tensor.cpp:227-254, engine_split.cpp:13-37).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <utility>
 
 #include "tsk_common.cuh"
@@ -117,7 +119,7 @@ __device__ __forceinline__ void fft_col(typename cx<T>::t (&v)[R], typename cx<T
 // ---- K1 / K3 ------------------------------------------------------------------
 
 template <typename T, int N, int R, int W, int MODE>
-__global__ void __launch_bounds__(N / R * W) k_wide(tsk_axis p)
+__global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * W) : 1) k_wide(tsk_axis p)
 {
     using T2 = typename cx<T>::t;
     using T4 = typename tw4<T>::t;
@@ -246,10 +248,10 @@ __global__ void __launch_bounds__(N / R * W) k_wide(tsk_axis p)
     }
 }
 
-template <typename T, int N>
+template <typename T, int N, int SEG = 256>
 struct Geom {
-    // 256-byte row segments; R elements per thread
-    static constexpr int W = 256 / (int)sizeof(typename cx<T>::t);
+    // SEG-byte row segments; R elements per thread
+    static constexpr int W = SEG / (int)sizeof(typename cx<T>::t);
     static constexpr int R = N >= 512 ? 32 : (N >= 128 ? 16 : 8);
     static constexpr int NT = N / R * W;
 };
@@ -262,10 +264,10 @@ static int sm_count()
     return sms > 0 ? sms : 148;
 }
 
-template <typename T, int N, int MODE>
+template <typename T, int N, int MODE, int SEG>
 static int launch(const tsk_axis& a, cudaStream_t st)
 {
-    using G = Geom<T, N>;
+    using G = Geom<T, N, SEG>;
     using T2 = typename cx<T>::t;
     if (G::NT > 1024 || a.inner % G::W != 0)
         return -1;
@@ -291,16 +293,32 @@ static int launch(const tsk_axis& a, cudaStream_t st)
     return (int)cudaGetLastError();
 }
 
+static int seg_bytes()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TSK_WIDE_SEG");
+        v = (e && atoi(e) == 128) ? 128 : 256;
+    }
+    return v;
+}
+
+template <typename T, int MODE, int SEG>
+static int dispatch_seg(const tsk_axis& a, cudaStream_t st)
+{
+    switch (a.n) {
+    case 64: return launch<T, 64, MODE, SEG>(a, st);
+    case 128: return launch<T, 128, MODE, SEG>(a, st);
+    case 256: return launch<T, 256, MODE, SEG>(a, st);
+    case 512: return launch<T, 512, MODE, SEG>(a, st);
+    default: return -1;
+    }
+}
+
 template <typename T, int MODE>
 static int dispatch(const tsk_axis& a, cudaStream_t st)
 {
-    switch (a.n) {
-    case 64: return launch<T, 64, MODE>(a, st);
-    case 128: return launch<T, 128, MODE>(a, st);
-    case 256: return launch<T, 256, MODE>(a, st);
-    case 512: return launch<T, 512, MODE>(a, st);
-    default: return -1;
-    }
+    return seg_bytes() == 128 ? dispatch_seg<T, MODE, 128>(a, st) : dispatch_seg<T, MODE, 256>(a, st);
 }
 
 }  // namespace wide
