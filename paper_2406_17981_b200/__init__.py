@@ -18,7 +18,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtoesplit.so.1")
+# TSK_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("TSK_LIB") or os.path.join(HERE, "libtoesplit.so.1")
 
 TS_OK = 0
 TS_ERR_INVALID_ARGUMENT, TS_ERR_SHAPE, TS_ERR_SYMMETRY, TS_ERR_CAP_EXCEEDED = 1, 2, 3, 4

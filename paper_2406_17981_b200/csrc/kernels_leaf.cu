@@ -117,9 +117,8 @@ __device__ __forceinline__ typename cx<T>::t cmac(typename cx<T>::t acc, typenam
                                                   typename cx<T>::t s, bool first)
 {
     if constexpr (sizeof(T) == 4) {
-        const float2 ix = mul2(swz(x), make_float2(-1.f, 1.f));
-        const float2 a = first ? mul2(bc_x(s), x) : fma2(bc_x(s), x, acc);
-        return fma2(bc_y(s), ix, a);
+        const float2 a = first ? mul2(x, bc_x(s)) : fma2(x, bc_x(s), acc);
+        return fma2(make_float2(-x.y, x.x), bc_y(s), a);
     } else {
         const typename cx<T>::t pr = cmul(x, s);
         return first ? pr : cadd(acc, pr);
