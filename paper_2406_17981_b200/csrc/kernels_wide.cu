@@ -118,6 +118,10 @@ __device__ __forceinline__ void fft_col(typename cx<T>::t (&v)[R], typename cx<T
 
 // ---- K1 / K3 ------------------------------------------------------------------
 
+#ifndef WIDE_K1_XTMEM
+#define WIDE_K1_XTMEM 0
+#endif
+
 template <typename T, int N, int R, int W, int MODE>
 __global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * W) : 1) k_wide(tsk_axis p)
 {
@@ -152,9 +156,11 @@ __global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * 
     constexpr int TCOLS = TCOLS_RAW <= 32 ? 32 : TCOLS_RAW <= 64 ? 64 : TCOLS_RAW <= 128 ? 128
                                                                         : TCOLS_RAW <= 256 ? 256 : 512;
     constexpr bool TM = PWORDS % 32 == 0;  // small R keeps B(e) in registers
-    const bool park = TM && MODE == 1 && ue && uo;
+    // K1 (WIDE_K1_XTMEM) keeps x in tensor memory for the even child instead
+    // of re-reading it through L2
+    const bool park = TM && (MODE == 1 || WIDE_K1_XTMEM) && ue && uo;
     uint32_t tbase = 0, lane_base = 0;
-    if constexpr (MODE == 1) {
+    if constexpr (MODE == 1 || WIDE_K1_XTMEM) {
         if (park) {
             tbase = tmem_alloc(&tmem_slot, TCOLS);
             const int warp = threadIdx.x / 32;
@@ -177,7 +183,14 @@ __global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * 
             if (uo) {
 #pragma unroll
                 for (int m = 0; m < R; ++m)
-                    v[m] = cmul_tw<T, false>(src[m * rs], load_tw<T>(ph + t + m * TF));
+                    v[m] = src[m * rs];
+                if constexpr (WIDE_K1_XTMEM && TM) {
+                    if (park)
+                        tmem_park<T, R>(lane_base, v);
+                }
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    v[m] = cmul_tw<T, false>(v[m], load_tw<T>(ph + t + m * TF));
                 fft_col<T, N, R, W, false>(v, buf, tw, t, w);
                 T2* dd = static_cast<T2*>(p.dst1) + base;
 #pragma unroll
@@ -185,9 +198,17 @@ __global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * 
                     dd[m * rs] = v[m];
             }
             if (ue) {
+                bool have = false;
+                if constexpr (WIDE_K1_XTMEM && TM) {
+                    if (park) {
+                        tmem_restore<T, R>(lane_base, v);
+                        have = true;
+                    }
+                }
+                if (!have)
 #pragma unroll
-                for (int m = 0; m < R; ++m)
-                    v[m] = src[m * rs];
+                    for (int m = 0; m < R; ++m)
+                        v[m] = src[m * rs];
                 fft_col<T, N, R, W, false>(v, buf, tw, t, w);
                 T2* de = static_cast<T2*>(p.dst0) + base;
 #pragma unroll
@@ -242,7 +263,7 @@ __global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * 
             }
         }
     }
-    if constexpr (MODE == 1) {
+    if constexpr (MODE == 1 || WIDE_K1_XTMEM) {
         if (park)
             tmem_free(tbase, TCOLS);
     }
@@ -293,14 +314,19 @@ static int launch(const tsk_axis& a, cudaStream_t st)
     return (int)cudaGetLastError();
 }
 
-static int seg_bytes()
+// Row segment per tile: K1 (one input, two outputs) runs two 128-byte-wide
+// CTAs per SM, K3 (two inputs) one 256-byte-wide CTA; TSK_WIDE_SEG=128|256
+// overrides both (A/B).
+static int seg_bytes(int mode)
 {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("TSK_WIDE_SEG");
-        v = (e && atoi(e) == 128) ? 128 : 256;
+        v = e ? atoi(e) : 0;
     }
-    return v;
+    if (v == 128 || v == 256)
+        return v;
+    return mode == 0 ? 128 : 256;
 }
 
 template <typename T, int MODE, int SEG>
@@ -318,7 +344,7 @@ static int dispatch_seg(const tsk_axis& a, cudaStream_t st)
 template <typename T, int MODE>
 static int dispatch(const tsk_axis& a, cudaStream_t st)
 {
-    return seg_bytes() == 128 ? dispatch_seg<T, MODE, 128>(a, st) : dispatch_seg<T, MODE, 256>(a, st);
+    return seg_bytes(MODE) == 128 ? dispatch_seg<T, MODE, 128>(a, st) : dispatch_seg<T, MODE, 256>(a, st);
 }
 
 }  // namespace wide
