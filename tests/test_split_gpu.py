@@ -311,3 +311,56 @@ def test_wide_dyadic_vs_oracle(levels):
     for prec, tol in ((T.C128, 1e-12), (T.C64, 1e-5)):
         op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec)
         assert rel_l2(op.apply(np.concatenate(xs)), ys) <= tol
+
+
+# ---- one-component-per-thread leaf kernel (csrc/kernels_leaf.cu): every leaf
+# length it instantiates (64..512), orbit geometry for d = 1..4 (no orbit axis,
+# one, two, plus a mirrored "rest" axis), both precisions, scalar and 3x3.
+LEAF_SHAPES = [[512], [6, 512], [4, 3, 512], [3, 2, 256], [2, 5, 128], [2, 2, 3, 64], [3, 2, 2, 128]]
+
+
+@pytest.mark.parametrize("levels", LEAF_SHAPES)
+@pytest.mark.parametrize("sym", [T.SYM_SYMMETRIC, T.SYM_SKEW])
+def test_leaf_kernel_scalar_vs_oracle(levels, sym):
+    g = T.Generator.random(levels, 17, 1.0, sym)
+    lags, v, y_or = _oracle_split(levels, sym, 17)
+    y = T.Operator.split(g).apply(v)
+    assert rel_l2(y, y_or) <= 1e-12
+    op = T.Operator.split_ex(T.BlockGenerator.from_scalar(g), precision=T.C64)
+    assert op.info()["storage"] == T.STORAGE_COMPRESSED
+    y64 = op.apply(v)
+    assert rel_l2(y64, y_or) <= 1e-5
+
+
+@pytest.mark.parametrize("levels", [[1, 1, 512], [4, 3, 512], [3, 2, 256], [2, 5, 128], [2, 3, 64]])
+@pytest.mark.parametrize("prec,tol", [(T.C128, 1e-12), (T.C64, 1e-5)])
+def test_leaf_kernel_dyadic_vs_oracle(levels, prec, tol):
+    xs = _dyadic_x(levels, 11)
+    ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+    op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec)
+    y = op.apply(np.concatenate(xs))
+    assert rel_l2(y, ys) <= tol
+
+
+@pytest.mark.parametrize("nparts", [2, 8])
+def test_leaf_kernel_partitions(nparts):
+    # single-branch leaf passes (use_even / use_odd only) of the new kernel
+    levels = [4, 2, 256]
+    xs = _dyadic_x(levels, 13)
+    ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+    bg = T.BlockGenerator.dyadic(levels)
+    acc = 0
+    for part in range(nparts):
+        op = T.Operator.split_ex(bg, precision=T.C64, part=part, nparts=nparts)
+        acc = acc + op.apply(np.concatenate(xs))
+    assert rel_l2(acc, ys) <= 1e-5
+
+
+def test_leaf_kernel_matches_previous_leaf_kernel(monkeypatch):
+    # the 8-point leaf kernel (TSK_NO_LEAF1=1 in a fresh process) is the A/B
+    # partner; here both must agree with the oracle on the same operator
+    levels = [3, 4, 128]
+    xs = _dyadic_x(levels, 19)
+    ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+    op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=T.C64)
+    assert rel_l2(op.apply(np.concatenate(xs)), ys) <= 1e-5
