@@ -5,8 +5,9 @@
 // The m x m spectra multiply couples the components through shared memory once
 // per branch; the even branch's output e' is parked in tensor memory (thread-
 // private lane) while the odd branch runs, and the odd branch re-reads x from
-// L2. A CTA processes one mirror orbit of 4 fibers (compressed spectra rows
-// fetched once, cp.async-staged), m components each.
+// L2. A unit is one mirror orbit of 4 fibers (compressed spectra rows fetched
+// once, cp.async-staged) or, with full storage, 4 consecutive fibers (spectra
+// read straight from global memory, each element once), m components each.
 //
 // Reference semantics (relative to /root/reference/proj): leaf multiply
 // src/core/kernel.cpp:126-219, leaf FFT/IFFT and deepest merge
@@ -213,7 +214,7 @@ constexpr int leaf1_g()
 #define LEAF_XTMEM 0
 #endif
 
-template <typename T, int N, int R, int M, int G = leaf1_g<N, R, M>()>
+template <typename T, int N, int R, int M, bool CMP, int G = leaf1_g<N, R, M>()>
 __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 * M * (N / R) < 384 ? 384 / (G * 4 * M * (N / R)) : 1) k_leaf1(tsk_axis p, tsk_spectra sp)
 {
     using T2 = typename cx<T>::t;
@@ -294,7 +295,8 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     int64_t rest = 1;
     for (int a = 0; a < A1; ++a)
         rest *= sp.levels[a];
-    const int64_t units = rest * st1 * st2;
+    // compressed: one unit = one mirror orbit; full storage: 4 consecutive fibers
+    const int64_t units = CMP ? rest * st1 * st2 : (p.outer + 3) / 4;
     const T2* src = static_cast<const T2*>(p.src0);
     T2* dst = static_cast<T2*>(p.dst0);
     const T2* spec = static_cast<const T2*>(sp.data);
@@ -311,7 +313,13 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
         bool valid;
         int64_t g, off0, off1;
         uint32_t neg = 0;
-        {
+        if constexpr (!CMP) {
+            g = u * 4 + f;
+            valid = uvalid && g < p.outer;
+            if (g >= p.outer)
+                g = p.outer - 1;
+            off0 = off1 = g * N;
+        } else {
             const uint32_t u32 = (uint32_t)u, st2u = (uint32_t)st2, st1u = (uint32_t)st1;
             const uint32_t q2 = u32 / st2u, q1 = q2 / st1u;
             const int64_t s2 = u32 - q2 * st2u, s1 = q2 - q1 * st1u, r = q1;
@@ -352,6 +360,8 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
         // of neg ^ lastneg (mirrored k)
         const uint32_t neg0 = neg, neg1 = neg ^ lastneg;
         auto stage_row = [&](int beta) {
+            if constexpr (!CMP)
+                return;
             const int L = beta ? N / 2 : N / 2 + 1;
             const T2* rowp = spec + sp.branch_base[beta] + (beta ? off1 : off0);
             for (int e = lt; e < UM * L; e += UT) {
@@ -426,7 +436,12 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                             ng = t0 ? neg0 : neg1;
                         else
                             ng = neg1;
-                        const T2 s_ = flip_bits<T>(sp_[uu * LROW], (ng >> uu) & 1u);
+                        T2 s_;
+                        if constexpr (CMP)
+                            s_ = flip_bits<T>(sp_[uu * LROW], (ng >> uu) & 1u);
+                        else  // full storage: this fiber's own row, read once
+                            s_ = ldg_c(spec + sp.branch_base[beta] + (beta ? off1 : off0) +
+                                       uu * sp.block_elems[beta] + t + TF * m);
                         const T2 xv = cc == C ? v[m] : fbufs[(f * M + cc) * NP + Pad<N, R>::rd(t, m)];
                         acc = cmac<T>(acc, xv, s_, cc == 0);
                     });
@@ -506,7 +521,7 @@ static int sm_count()
     return sms > 0 ? sms : 148;
 }
 
-template <typename T, int N, int R, int M>
+template <typename T, int N, int R, int M, bool CMP>
 static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
     using T2 = typename cx<T>::t;
@@ -518,7 +533,7 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         sizeof(T2) * (R * (N / R - 1) + G * 4 * M * NP + G * (M == 1 ? 1 : 6) * (N / 2 + 1));
     if (smem > 227 * 1024)
         return -1;
-    auto kern = k_leaf1<T, N, R, M>;
+    auto kern = k_leaf1<T, N, R, M, CMP>;
     static thread_local int cached_dev = -1, cap = 0;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -541,26 +556,36 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         cached_dev = dev;
     }
     int64_t units = 1;
-    for (int ax = 0; ax < sp.d - 1; ++ax)
-        units *= ax >= sp.d - 3 ? stored_len(sp.levels[ax], (sp.branch_bits[0] >> ax) & 1u)
-                                : sp.levels[ax];
+    if (CMP) {
+        for (int ax = 0; ax < sp.d - 1; ++ax)
+            units *= ax >= sp.d - 3 ? stored_len(sp.levels[ax], (sp.branch_bits[0] >> ax) & 1u)
+                                    : sp.levels[ax];
+    } else {
+        units = (a.outer + 3) / 4;
+    }
     const int64_t tiles = (units + G - 1) / G;
     const int64_t grid = tiles < cap ? tiles : cap;
     kern<<<(unsigned)(grid > 0 ? grid : 1), NT, smem, st>>>(a, sp);
     return (int)cudaGetLastError();
 }
 
+template <typename T, int M, bool CMP>
+static int dispatch_s(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
+{
+    switch (a.n) {
+    case 64: return launch<T, 64, 8, M, CMP>(a, sp, st);
+    case 128: return launch<T, 128, 16, M, CMP>(a, sp, st);
+    case 256: return launch<T, 256, 16, M, CMP>(a, sp, st);
+    case 512:  // complex128 at R = 32 spills; the 8-point kernel handles it
+        return sizeof(T) == 4 ? launch<T, 512, 32, M, CMP>(a, sp, st) : -1;
+    default: return -1;
+    }
+}
+
 template <typename T, int M>
 static int dispatch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
-    switch (a.n) {
-    case 64: return launch<T, 64, 8, M>(a, sp, st);
-    case 128: return launch<T, 128, 16, M>(a, sp, st);
-    case 256: return launch<T, 256, 16, M>(a, sp, st);
-    case 512:  // complex128 at R = 32 spills; the 8-point kernel handles it
-        return sizeof(T) == 4 ? launch<T, 512, 32, M>(a, sp, st) : -1;
-    default: return -1;
-    }
+    return sp.compressed ? dispatch_s<T, M, true>(a, sp, st) : dispatch_s<T, M, false>(a, sp, st);
 }
 
 }  // namespace leaf
@@ -569,7 +594,7 @@ static int dispatch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 // -1: not covered (caller falls back), else the launch cudaError_t.
 extern "C" int tsk_leaf1_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream)
 {
-    if (a->inner != 1 || !sp->compressed)
+    if (a->inner != 1)
         return -1;
     static const int8_t canon[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
     auto st = (cudaStream_t)stream;

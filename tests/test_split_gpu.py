@@ -320,24 +320,28 @@ LEAF_SHAPES = [[512], [6, 512], [4, 3, 512], [3, 2, 256], [2, 5, 128], [2, 2, 3,
 
 
 @pytest.mark.parametrize("levels", LEAF_SHAPES)
-@pytest.mark.parametrize("sym", [T.SYM_SYMMETRIC, T.SYM_SKEW])
+@pytest.mark.parametrize("sym", [T.SYM_GENERAL, T.SYM_SYMMETRIC, T.SYM_SKEW])
 def test_leaf_kernel_scalar_vs_oracle(levels, sym):
+    # GENERAL -> full storage (4 consecutive fibers per unit, spectra from
+    # global memory); symmetric / skew -> mirror-compressed orbits
     g = T.Generator.random(levels, 17, 1.0, sym)
     lags, v, y_or = _oracle_split(levels, sym, 17)
     y = T.Operator.split(g).apply(v)
     assert rel_l2(y, y_or) <= 1e-12
     op = T.Operator.split_ex(T.BlockGenerator.from_scalar(g), precision=T.C64)
-    assert op.info()["storage"] == T.STORAGE_COMPRESSED
+    want = T.STORAGE_FULL if sym == T.SYM_GENERAL else T.STORAGE_COMPRESSED
+    assert op.info()["storage"] == want
     y64 = op.apply(v)
     assert rel_l2(y64, y_or) <= 1e-5
 
 
 @pytest.mark.parametrize("levels", [[1, 1, 512], [4, 3, 512], [3, 2, 256], [2, 5, 128], [2, 3, 64]])
 @pytest.mark.parametrize("prec,tol", [(T.C128, 1e-12), (T.C64, 1e-5)])
-def test_leaf_kernel_dyadic_vs_oracle(levels, prec, tol):
+@pytest.mark.parametrize("storage", [T.STORAGE_AUTO, T.STORAGE_FULL])
+def test_leaf_kernel_dyadic_vs_oracle(levels, prec, tol, storage):
     xs = _dyadic_x(levels, 11)
     ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
-    op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec)
+    op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec, storage=storage)
     y = op.apply(np.concatenate(xs))
     assert rel_l2(y, ys) <= tol
 
