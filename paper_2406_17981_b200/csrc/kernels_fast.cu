@@ -24,7 +24,6 @@
 #include <type_traits>
 
 #include "tsk_common.cuh"
-#include "tsk_tmem.cuh"
 
 namespace tsk {
 namespace fast {
@@ -614,18 +613,9 @@ __device__ __forceinline__ void matvec3(typename cx<T>::t (&x)[3], const typenam
 // fibers. Components are transformed one after another through a single pair
 // of exchange buffers; the m x m multiply happens in registers. The leaf
 // parities along the last axis are even (beta 0) and odd (beta 1).
-template <typename T, int N, int M, int G, bool DBG = false>
-__global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(tsk_axis p, tsk_spectra sp,
-                                                                             unsigned long long* dbg = nullptr)
+template <typename T, int N, int M, int G>
+__global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(tsk_axis p, tsk_spectra sp)
 {
-    // DBG: per-phase clock64 accounting of thread 0 (tools: TSK_PHASE_DEBUG=1)
-    unsigned long long dacc[12] = {0}, dlast = 0;
-#define TSK_T(i)                                      \
-    if (DBG && threadIdx.x == 0) {                    \
-        const unsigned long long c_ = clock64();      \
-        dacc[i] += c_ - dlast;                        \
-        dlast = c_;                                   \
-    }
     using T2 = typename cx<T>::t;
     using T4 = typename tw4<T>::t;
     using PL = Plan<N>;
@@ -707,8 +697,6 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
     T2* stash_me = stash + slot * N + t;
     int xc = 0;
 
-    if (DBG && threadIdx.x == 0)
-        dlast = clock64();
     for (int64_t tile = blockIdx.x; tile * G < units; tile += gridDim.x) {
         const int64_t u = tile * G + gi;
         bool valid = false;
@@ -783,7 +771,6 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
         // every member thread computed the same unit row; slot-0 threads hold it
         // whether or not their own fiber is valid (row offsets depend on the unit)
         stage(p.use_even ? 0 : 1);
-        TSK_T(0);
         T2 v[M][8];
 #pragma unroll
         for (int beta = 0; beta < 2; ++beta) {
@@ -813,19 +800,16 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
                         v[c][m] = phr.template apply<false>(x, m);
                     }
                 }
-            TSK_T(1 + 5 * beta);
 #pragma unroll
             for (int c = 0; c < M; ++c)
                 fft_rows<T, N, false, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, LEAF_REGTW, Tw<T>[NWR]>(
                     *reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx, tw, t, xc, fsync, wreg);
-            TSK_T(2 + 5 * beta);
             const T2* sb = static_cast<const T2*>(sp.data) + sp.branch_base[beta] + off[beta];
             const int64_t bst = sp.block_elems[beta];
             if (compressed) {
                 cp_async_wait_all();
                 __syncthreads();  // the staged row is complete and visible
             }
-            TSK_T(3 + 5 * beta);
             constexpr int MB = 1;  // frequencies per spectra batch
 #pragma unroll
             for (int mb = 0; mb < 8; mb += MB) {
@@ -893,7 +877,6 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
                 // spectra values held in registers (all 48 at once spills)
                 asm volatile("" ::: "memory");
             }
-            TSK_T(4 + 5 * beta);
             if (compressed) {
                 __syncthreads();  // everyone is done with the staged row
                 if (beta == 0 && p.use_odd)
@@ -903,7 +886,6 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
             for (int c = 0; c < M; ++c)
                 fft_rows<T, N, true, 1, FiberIdx<N, sizeof(T2)>, SyncGroup, LEAF_REGTW, Tw<T>[NWR]>(
                     *reinterpret_cast<T2(*)[1][8]>(&v[c]), buf0, buf1, sidx, tw, t, xc, fsync, wreg);
-            TSK_T(5 + 5 * beta);
         }
         if (valid) {
             T2* yout = dst + g * N + t;
@@ -923,299 +905,6 @@ __global__ void __launch_bounds__(N / 8 * 4 * G, sizeof(T) == 4 ? 2 : 1) k_leaf(
                 }
         }
     }
-    if (DBG && threadIdx.x == 0 && dbg)
-        for (int i = 0; i < 12; ++i)
-            atomicAdd(dbg + i, dacc[i]);
-#undef TSK_T
-}
-
-template <typename T, int N, int M, int G>
-__global__ void __launch_bounds__(N / 8 * 4 * G, 1) k_leaf_ilp(tsk_axis p, tsk_spectra sp, unsigned long long* = nullptr)
-{
-    using T2 = typename cx<T>::t;
-    using T4 = typename tw4<T>::t;
-    using PL = Plan<N>;
-    constexpr int TF = PL::TF;
-    constexpr int S = 4 * G;  // fiber slots per CTA
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T4* twt = reinterpret_cast<T4*>(smem_raw);
-    T2* buf0 = reinterpret_cast<T2*>(twt + PL::TW);  // M x S x N, ping-pong
-    T2* buf1 = buf0 + M * S * N;
-    // compressed spectra: one branch's stored row of every unique component,
-    // per unit, staged with cp.async while the forward transforms run
-    constexpr int LROW = N / 2 + 1;
-    constexpr int UM = M == 1 ? 1 : 6;
-    T2* sstage = buf1 + M * S * N;  // G x UM x LROW
-    // thread-private stash in tensor memory: x (even branch), then e'
-    __shared__ uint32_t tmem_slot;
-    constexpr int W8 = 8 * (int)sizeof(T2) / 4;
-    constexpr int NWARP = N / 8 * 4 * G / 32;
-    constexpr int TCOLS = tmem_cols_pow2(M * W8 * ((NWARP + 3) / 4));
-    const uint32_t tbase = tmem_alloc(&tmem_slot, TCOLS);
-    const uint32_t lane_base = tbase + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16) +
-                               (uint32_t)(M * W8 * ((threadIdx.x / 32) / 4));
-    {
-        // stage tables only (the phase comes from registers)
-#pragma unroll
-        for (int s = 1; s < PL::NST; ++s) {
-            const int pr = PL::radix(s), ns = PL::ns(s);
-            for (int e = threadIdx.x; e < ns * (pr - 1); e += blockDim.x) {
-                const int jm = e / (pr - 1), r = e % (pr - 1) + 1;
-                twt[PL::tw_off(s) + e] =
-                    make_tw<T>(ldg_c(static_cast<const T2*>(p.roots) + (r * jm * (N / (ns * pr))) % N));
-            }
-        }
-        __syncthreads();
-    }
-
-    const int slot = threadIdx.x / TF;
-    const int gi = slot / 4, f = slot % 4;
-    const int t = threadIdx.x % TF;
-    // per-thread twiddle bases and split phase, loaded once (no table reads
-    // inside the transforms)
-    // per-thread twiddle bases of the last stage (powers in registers)
-    constexpr int SL = PL::NST - 1;
-    constexpr int NWR = SL > 0 ? 8 / PL::radix(SL) : 1;
-    Tw<T> wreg[NWR];
-    if constexpr (SL > 0) {
-        const T2* roots = static_cast<const T2*>(p.roots);
-        constexpr int pr = PL::radix(SL), ns = PL::ns(SL);
-#pragma unroll
-        for (int i = 0; i < NWR; ++i) {
-            const int jm = (t + i * TF) % ns;
-            wreg[i] = make_twv<T>(ldg_c(roots + jm * (N / (ns * pr))));
-        }
-    }
-    PhaseReg<T> phr;
-    phr.pt = make_twv<T>(ldg_c(static_cast<const T2*>(p.phase) + t));
-    const typename tw4<T>::t* tw = twt;
-    constexpr int FT = TF;  // threads per fiber; exchanges sync only those
-    const SyncGroup fsync{1 + (int)(threadIdx.x / (FT >= 32 ? FT : 32)), FT >= 32 ? FT : 32};
-    const int ut = threadIdx.x - gi * 4 * TF;  // thread index within the unit
-    const T scale = (T)p.scale;
-    const T2* src = static_cast<const T2*>(p.src0);
-    T2* dst = static_cast<T2*>(p.dst0);
-    FiberIdx<N, sizeof(T2)> sidx{slot * N, S * N};
-    const int d = sp.d;
-    const int U = sp.n_unique;
-    const bool compressed = sp.compressed;
-    const uint32_t bits = sp.branch_bits[0];  // outer-axis parities (shared by both leaves)
-    uint32_t lastneg = 0;                     // components skew along the leaf axis
-    for (int uu = 0; uu < U; ++uu)
-        lastneg |= ((sp.skew_mask[uu] >> (d - 1)) & 1u) << uu;
-    // orbit axes (last two outer axes) and unit count
-    const int A2 = d - 2, A1 = d - 3;
-    int64_t n1 = 1, n2 = 1, st1 = 1, st2 = 1, rest = 1;
-    if (A2 >= 0) {
-        n2 = sp.levels[A2];
-        st2 = compressed ? stored_len(n2, (bits >> A2) & 1u) : n2;
-    }
-    if (A1 >= 0) {
-        n1 = sp.levels[A1];
-        st1 = compressed ? stored_len(n1, (bits >> A1) & 1u) : n1;
-    }
-    for (int a = 0; a < A1; ++a)
-        rest *= sp.levels[a];
-    const int64_t units = compressed ? rest * st1 * st2 : (p.outer + 3) / 4;
-    int xc = 0;
-
-    for (int64_t tile = blockIdx.x; tile * G < units; tile += gridDim.x) {
-        const int64_t u = tile * G + gi;
-        bool valid = false;
-        int64_t g = 0, off[2] = {0, 0};
-        uint32_t neg = 0;
-        if (u < units) {
-            if (!compressed) {
-                g = u * 4 + f;
-                valid = g < p.outer;
-                off[0] = off[1] = g * N;
-            } else {
-                const int64_t s2 = u % st2;
-                const int64_t s1 = (u / st2) % st1;
-                const int64_t r = u / (st2 * st1);
-                int64_t p1 = 0, p2 = 0;
-                const int c1 = A1 >= 0 ? orbit_members(n1, (bits >> A1) & 1u, s1, p1) : 1;
-                const int c2 = A2 >= 0 ? orbit_members(n2, (bits >> A2) & 1u, s2, p2) : 1;
-                {
-                    valid = f < c1 * c2;
-                    const int i1 = (f % (c1 * c2)) / c2, i2 = f % c2;
-                    const int64_t kk1 = A1 < 0 ? 0 : (i1 ? p1 : s1);
-                    const int64_t kk2 = A2 < 0 ? 0 : (i2 ? p2 : s2);
-                    for (int uu = 0; uu < U; ++uu) {
-                        if (A1 >= 0 && i1)
-                            neg ^= ((sp.skew_mask[uu] >> A1) & 1u) << uu;
-                        if (A2 >= 0 && i2)
-                            neg ^= ((sp.skew_mask[uu] >> A2) & 1u) << uu;
-                    }
-                    // rest axes (0 .. d-4): plain per-fiber mirror remap
-                    int64_t rsrc = 0, rstride_elems = 1, gr = r, rfull = 0, rmul = 1;
-                    for (int a = A1 - 1; a >= 0; --a) {
-                        const int64_t na = sp.levels[a];
-                        const int64_t ka = gr % na;
-                        gr /= na;
-                        const int odd = (bits >> a) & 1u;
-                        bool mm;
-                        rsrc += mirror_src(na, odd, ka, mm) * rstride_elems;
-                        rstride_elems *= stored_len(na, odd);
-                        rfull += ka * rmul;
-                        rmul *= na;
-                        if (mm)
-                            for (int uu = 0; uu < U; ++uu)
-                                neg ^= ((sp.skew_mask[uu] >> a) & 1u) << uu;
-                    }
-                    g = (rfull * n1 + kk1) * n2 + kk2;
-                    const int64_t row = (rsrc * st1 + s1) * st2 + s2;
-                    off[0] = row * (N / 2 + 1);
-                    off[1] = row * (N / 2);
-                }
-            }
-        }
-        const T2* xin = src + g * N + t;
-        T2* stg = sstage + gi * UM * LROW;
-        auto stage = [&](int beta) {
-            if (!compressed || u >= units)
-                return;
-            const int L = beta ? N / 2 : N / 2 + 1;
-            const T2* row = static_cast<const T2*>(sp.data) + sp.branch_base[beta] + off[beta];
-            for (int e = ut; e < UM * L; e += 4 * TF) {
-                const int uu = e / L, kk = e - uu * L;
-                if constexpr (sizeof(T2) == 8)
-                    cp_async8(stg + uu * LROW + kk, row + uu * sp.block_elems[beta] + kk);
-                else
-                    cp_async16(stg + uu * LROW + kk, row + uu * sp.block_elems[beta] + kk);
-            }
-            cp_async_commit();
-        };
-        // every member thread computed the same unit row; slot-0 threads hold it
-        // whether or not their own fiber is valid (row offsets depend on the unit)
-        stage(p.use_even ? 0 : 1);
-        T2 v[M][8];
-#pragma unroll
-        for (int beta = 0; beta < 2; ++beta) {
-            const bool use = beta ? p.use_odd : p.use_even;
-            if (!use)
-                continue;
-            if (beta == 1 && p.use_even) {
-                // x from the stash, e' into it
-                T2 x[M][8];
-                tmem_wait_st();
-#pragma unroll
-                for (int c = 0; c < M; ++c)
-                    tmem_get8(lane_base, c * W8, x[c]);
-#pragma unroll
-                for (int c = 0; c < M; ++c)
-                    tmem_put8(lane_base, c * W8, v[c]);
-#pragma unroll
-                for (int c = 0; c < M; ++c)
-#pragma unroll
-                    for (int m = 0; m < 8; ++m)
-                        v[c][m] = phr.template apply<false>(x[c][m], m);
-            } else {
-#pragma unroll
-                for (int c = 0; c < M; ++c)
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) {
-                        T2 x = make_c<T>(0, 0);
-                        if (valid)
-                            x = xin[c * p.cstride + m * TF];
-                        v[c][m] = beta ? phr.template apply<false>(x, m) : x;
-                    }
-                if (beta == 0 && p.use_odd) {
-#pragma unroll
-                    for (int c = 0; c < M; ++c)
-                        tmem_put8(lane_base, c * W8, v[c]);
-                }
-            }
-            fft_rows<T, N, false, M, FiberIdx<N, sizeof(T2)>, SyncGroup, true, Tw<T>[NWR], false>(
-                v, buf0, buf1, sidx, tw, t, xc, fsync, wreg);
-            const T2* sb = static_cast<const T2*>(sp.data) + sp.branch_base[beta] + off[beta];
-            const int64_t bst = sp.block_elems[beta];
-            if (compressed) {
-                cp_async_wait_all();
-                __syncthreads();  // the staged row is complete and visible
-            }
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const int k = t + m * TF;
-                int kidx = k;
-                bool mir = false;
-                if (compressed) {
-                    // beta 0: even parity (stores 0..N/2), beta 1: odd (0..N/2-1)
-                    if (beta == 0) {
-                        mir = k > N / 2;
-                        kidx = mir ? N - k : k;
-                    } else {
-                        mir = k >= N / 2;
-                        kidx = mir ? N - 1 - k : k;
-                    }
-                }
-                const uint32_t ng = neg ^ (mir ? lastneg : 0u);
-                if (M == 1) {
-                    T2 sv = make_c<T>(0, 0);
-                    if (compressed)
-                        sv = stg[kidx];
-                    else if (valid)
-                        sv = ldg_c(sb + kidx);
-                    sv = flip_sign(sv, ng & 1u);
-                    v[0][m] = cmul(v[0][m], sv);
-                } else {
-                    T2 sv[6];
-#pragma unroll
-                    for (int uu = 0; uu < 6; ++uu) {
-                        T2 s = make_c<T>(0, 0);
-                        if (compressed)
-                            s = stg[uu * LROW + kidx];
-                        else if (valid)
-                            s = ldg_c(sb + uu * bst + kidx);
-                        sv[uu] = flip_sign(s, (ng >> uu) & 1u);
-                    }
-                    T2 x[3] = {v[0][m], v[1][m], v[2][m]};
-                    matvec3<T>(x, sv);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c)
-                        v[c][m] = x[c];
-                }
-                // compiler barrier: keeps ptxas from hoisting all 8 x 6 spectra
-                // loads ahead of the arithmetic (that alone spills)
-                asm volatile("" ::: "memory");
-            }
-            if (compressed) {
-                __syncthreads();  // everyone is done with the staged row
-                if (beta == 0 && p.use_odd)
-                    stage(1);  // lands while this branch's inverse transforms run
-            }
-            fft_rows<T, N, true, M, FiberIdx<N, sizeof(T2)>, SyncGroup, true, Tw<T>[NWR], false>(
-                v, buf0, buf1, sidx, tw, t, xc, fsync, wreg);
-        }
-        {
-            // tcgen05.ld is warp-collective: every thread loads the stash
-            T2 e[M][8];
-            if (p.use_odd && p.use_even) {
-                tmem_wait_st();
-#pragma unroll
-                for (int c = 0; c < M; ++c)
-                    tmem_get8(lane_base, c * W8, e[c]);
-            }
-            if (valid) {
-                T2* yout = dst + g * N + t;
-#pragma unroll
-                for (int c = 0; c < M; ++c)
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) {
-                        T2 a;
-                        if (p.use_odd) {
-                            a = phr.template apply<true>(v[c][m], m);
-                            if (p.use_even)
-                                a = cadd(a, e[c][m]);
-                        } else {
-                            a = v[c][m];
-                        }
-                        yout[c * p.cstride + m * TF] = cscale<T>(a, scale);
-                    }
-            }
-        }
-    }
-    tmem_free(tbase, TCOLS);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -1280,66 +969,17 @@ static int launch_strided(const tsk_axis& a, cudaStream_t st)
     return (int)cudaGetLastError();
 }
 
-static bool leaf_ilp()
-{
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TSK_LEAF_ILP");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-
 template <typename T, int N, int M>
 static int launch_leaf(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
     constexpr int G = (N / 8 * 4 >= 256) ? 1 : 256 / (N / 8 * 4);
     constexpr int S = 4 * G;
     using T2 = typename cx<T>::t;
-    const bool ilp = leaf_ilp();
-    const size_t smem = ilp ? 2 * sizeof(T2) * Plan<N>::TW + sizeof(T2) * 2 * M * S * N +
-                                  sizeof(T2) * G * (M == 1 ? 1 : 6) * (N / 2 + 1)
-                            : 2 * sizeof(T2) * Plan<N>::TW + sizeof(T2) * (2 + M) * S * N +
-                                  sizeof(T2) * G * (M == 1 ? 1 : 6) * (N / 2 + 1);
+    const size_t smem = 2 * sizeof(T2) * Plan<N>::TW + sizeof(T2) * (2 + M) * S * N +
+                        sizeof(T2) * G * (M == 1 ? 1 : 6) * (N / 2 + 1);
     if (smem > 227 * 1024)
         return -1;
-    static const bool phase_dbg = [] {
-        const char* e = getenv("TSK_PHASE_DEBUG");
-        return e && e[0] == '1';
-    }();
-    if (phase_dbg && !ilp) {
-        auto kd = k_leaf<T, N, M, G, true>;
-        int capd = 0;
-        if (int e = prep(kd, smem, N / 8 * S, capd))
-            return e;
-        unsigned long long* dbg = nullptr;
-        cudaMalloc(&dbg, 12 * sizeof(unsigned long long));
-        cudaMemset(dbg, 0, 12 * sizeof(unsigned long long));
-        int64_t units = 1;
-        for (int ax = 0; ax < sp.d - 1; ++ax)
-            units *= (sp.compressed && ax >= sp.d - 3)
-                         ? stored_len(sp.levels[ax], (sp.branch_bits[0] >> ax) & 1u)
-                         : sp.levels[ax];
-        if (!sp.compressed)
-            units = (a.outer + 3) / 4;
-        const int64_t nt = (units + G - 1) / G;
-        kd<<<(unsigned)std::min<int64_t>(nt, capd), N / 8 * S, smem, st>>>(a, sp, dbg);
-        unsigned long long h[12];
-        cudaMemcpy(h, dbg, sizeof h, cudaMemcpyDeviceToHost);
-        cudaFree(dbg);
-        const char* names[12] = {"setup+stage", "x load/stash", "fwd FFT e", "spec wait e", "multiply e",
-                                 "inv FFT e", "odd load", "fwd FFT o", "spec wait o", "multiply o",
-                                 "inv FFT o", "-"};
-        unsigned long long tot = 0;
-        for (int i = 0; i < 12; ++i)
-            tot += h[i];
-        fprintf(stderr, "k_leaf<N=%d,M=%d> phases (thread 0, all CTAs):", N, M);
-        for (int i = 0; i < 11; ++i)
-            fprintf(stderr, " %s %.1f%%", names[i], 100.0 * h[i] / (tot ? tot : 1));
-        fprintf(stderr, "\n");
-        return (int)cudaGetLastError();
-    }
-    auto kern = ilp ? k_leaf_ilp<T, N, M, G> : k_leaf<T, N, M, G>;
+    auto kern = k_leaf<T, N, M, G>;
     int cap = 0;
     if (int e = prep(kern, smem, N / 8 * S, cap))
         return e;
@@ -1358,7 +998,7 @@ static int launch_leaf(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st
     }
     const int64_t ntiles = (units + G - 1) / G;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, cap));
-    kern<<<(unsigned)grid, N / 8 * S, smem, st>>>(a, sp, nullptr);
+    kern<<<(unsigned)grid, N / 8 * S, smem, st>>>(a, sp);
     return (int)cudaGetLastError();
 }
 

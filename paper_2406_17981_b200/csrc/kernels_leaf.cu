@@ -210,10 +210,6 @@ constexpr int leaf1_g()
     return 128 / gcd_i(128, 4 * M * (N / R));
 }
 
-#ifndef LEAF_XTMEM
-#define LEAF_XTMEM 0
-#endif
-
 template <typename T, int N, int R, int M, bool CMP, int G = leaf1_g<N, R, M>()>
 __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 * M * (N / R) < 384 ? 384 / (G * 4 * M * (N / R)) : 1) k_leaf1(tsk_axis p, tsk_spectra sp)
 {
@@ -260,16 +256,13 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     // e' parked in TMEM when it is a multiple of 32 words, else in registers
     constexpr int EW = R * (int)sizeof(T2) / 4;
     constexpr bool TM = EW % 32 == 0;
-    constexpr bool XT = TM && LEAF_XTMEM;
     constexpr int NW = NT / 32 > 0 ? NT / 32 : 1;
-    // per thread: e' (EW words) and, with XT, a copy of x for the odd branch
-    constexpr int SW = XT ? 2 * EW : EW;
-    constexpr int TCOLS = tmem_cols_pow2(SW * ((NW + 3) / 4));
+    constexpr int TCOLS = tmem_cols_pow2(EW * ((NW + 3) / 4));
     uint32_t tbase = 0, lane_base = 0;
     if constexpr (TM) {
         tbase = tmem_alloc(&tmem_slot, TCOLS);
         lane_base = tbase + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16) +
-                    (uint32_t)(SW * ((threadIdx.x / 32) / 4));
+                    (uint32_t)(EW * ((threadIdx.x / 32) / 4));
     } else {
         __syncthreads();
     }
@@ -380,23 +373,12 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
         for (int beta = 0; beta < 2; ++beta) {
             if (beta == 0 ? !ue : !uo)
                 continue;
+            // x; the odd branch re-reads it (an L1 hit: the CTA's x rows fit next
+            // to its shared memory; measured faster than a TMEM copy)
             T2 v[R];
-            bool have = false;
-            if constexpr (XT) {
-                if (beta == 1 && both) {
-                    tmem_restore<T, R>(lane_base + EW, v);  // x kept from the even branch
-                    have = true;
-                }
-            }
-            if (!have) {
 #pragma unroll
-                for (int m = 0; m < R; ++m)
-                    v[m] = xin[m * TF];
-                if constexpr (XT) {
-                    if (beta == 0 && both)
-                        tmem_park<T, R>(lane_base + EW, v);
-                }
-            }
+            for (int m = 0; m < R; ++m)
+                v[m] = xin[m * TF];
             if (beta == 1)
                 sfor<0, R>([&](auto I) {
                     constexpr int mi = decltype(I)::value;
@@ -546,7 +528,7 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         // TMEM: every resident CTA allocates its columns
         constexpr int EW = R * (int)sizeof(T2) / 4;
         constexpr int NW = NT / 32 > 0 ? NT / 32 : 1;
-        constexpr int TC = tmem_cols_pow2((LEAF_XTMEM ? 2 : 1) * EW * ((NW + 3) / 4));
+        constexpr int TC = tmem_cols_pow2(EW * ((NW + 3) / 4));
         if (EW % 32 == 0 && per_sm * TC > 512)
             per_sm = 512 / TC;
         if (getenv("TSK_DEBUG_OCC"))

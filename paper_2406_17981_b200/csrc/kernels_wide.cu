@@ -118,10 +118,6 @@ __device__ __forceinline__ void fft_col(typename cx<T>::t (&v)[R], typename cx<T
 
 // ---- K1 / K3 ------------------------------------------------------------------
 
-#ifndef WIDE_K1_XTMEM
-#define WIDE_K1_XTMEM 0
-#endif
-
 template <typename T, int N, int R, int W, int MODE>
 __global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * W) : 1) k_wide(tsk_axis p)
 {
@@ -156,11 +152,9 @@ __global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * 
     constexpr int TCOLS = TCOLS_RAW <= 32 ? 32 : TCOLS_RAW <= 64 ? 64 : TCOLS_RAW <= 128 ? 128
                                                                         : TCOLS_RAW <= 256 ? 256 : 512;
     constexpr bool TM = PWORDS % 32 == 0;  // small R keeps B(e) in registers
-    // K1 (WIDE_K1_XTMEM) keeps x in tensor memory for the even child instead
-    // of re-reading it through L2
-    const bool park = TM && (MODE == 1 || WIDE_K1_XTMEM) && ue && uo;
+    const bool park = TM && MODE == 1 && ue && uo;
     uint32_t tbase = 0, lane_base = 0;
-    if constexpr (MODE == 1 || WIDE_K1_XTMEM) {
+    if constexpr (MODE == 1) {
         if (park) {
             tbase = tmem_alloc(&tmem_slot, TCOLS);
             const int warp = threadIdx.x / 32;
@@ -183,14 +177,7 @@ __global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * 
             if (uo) {
 #pragma unroll
                 for (int m = 0; m < R; ++m)
-                    v[m] = src[m * rs];
-                if constexpr (WIDE_K1_XTMEM && TM) {
-                    if (park)
-                        tmem_park<T, R>(lane_base, v);
-                }
-#pragma unroll
-                for (int m = 0; m < R; ++m)
-                    v[m] = cmul_tw<T, false>(v[m], load_tw<T>(ph + t + m * TF));
+                    v[m] = cmul_tw<T, false>(src[m * rs], load_tw<T>(ph + t + m * TF));
                 fft_col<T, N, R, W, false>(v, buf, tw, t, w);
                 T2* dd = static_cast<T2*>(p.dst1) + base;
 #pragma unroll
@@ -198,17 +185,10 @@ __global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * 
                     dd[m * rs] = v[m];
             }
             if (ue) {
-                bool have = false;
-                if constexpr (WIDE_K1_XTMEM && TM) {
-                    if (park) {
-                        tmem_restore<T, R>(lane_base, v);
-                        have = true;
-                    }
-                }
-                if (!have)
+                // x again (L1/L2 hit; measured faster than a TMEM copy)
 #pragma unroll
-                    for (int m = 0; m < R; ++m)
-                        v[m] = src[m * rs];
+                for (int m = 0; m < R; ++m)
+                    v[m] = src[m * rs];
                 fft_col<T, N, R, W, false>(v, buf, tw, t, w);
                 T2* de = static_cast<T2*>(p.dst0) + base;
 #pragma unroll
@@ -263,7 +243,7 @@ __global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * 
             }
         }
     }
-    if constexpr (MODE == 1 || WIDE_K1_XTMEM) {
+    if constexpr (MODE == 1) {
         if (park)
             tmem_free(tbase, TCOLS);
     }
