@@ -20,6 +20,8 @@
 #include <fstream>
 #include <map>
 #include <mutex>
+#include <thread>
+#include <vector>
 
 #include "host.hpp"
 #include "tsk_launch.h"
@@ -724,6 +726,154 @@ void apply_device(const DeviceOperator& op, const void* x, void* y, void* stream
         fill_counters(op, metrics);
 }
 
+
+// ---- host <-> device transfer of the reference ABI's interleaved complex128
+// buffers. Caller memory is pageable, so a single cudaMemcpy runs at the
+// driver's bounce-buffer rate; large transfers instead use T worker threads,
+// each with its own stream and two pinned 16 MB slots: a worker copies chunk
+// i into a pinned slot (host memcpy) while the DMA of its previous chunk is in
+// flight, and complex64 operators convert on the device per chunk.
+namespace {
+
+constexpr size_t kChunkElems = size_t(1) << 20;  // complex elements (16 MB as complex128)
+
+struct PinnedPool {
+    std::mutex mu;
+    std::vector<void*> free_;
+    void* get()
+    {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!free_.empty()) {
+                void* p = free_.back();
+                free_.pop_back();
+                return p;
+            }
+        }
+        void* p = nullptr;
+        cuda_check(cudaHostAlloc(&p, kChunkElems * 16, cudaHostAllocPortable), "cudaHostAlloc");
+        return p;
+    }
+    void put(void* p)
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        free_.push_back(p);
+    }
+};
+PinnedPool& pinned_pool()
+{
+    static PinnedPool* pool = new PinnedPool;  // process lifetime
+    return *pool;
+}
+
+int transfer_threads()
+{
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    return static_cast<int>(std::clamp(hw / 2, 2u, 8u));
+}
+
+// dir 0: host complex128 v -> device x (complex64 when c64); dir 1: device y
+// -> host complex128. Blocks until done; errors surface as TsError.
+void host_transfer(int dir, int device, double* host, void* dev, bool c64, int64_t count)
+{
+    const int64_t nchunks = (count + static_cast<int64_t>(kChunkElems) - 1) / static_cast<int64_t>(kChunkElems);
+    const int T = static_cast<int>(std::min<int64_t>(transfer_threads(), nchunks));
+    std::vector<std::thread> th;
+    std::vector<std::string> err(T);
+    for (int k = 0; k < T; ++k) {
+        th.emplace_back([&, k] {
+            cudaStream_t s = nullptr;
+            void* pin[2] = {nullptr, nullptr};
+            void* stage[2] = {nullptr, nullptr};
+            cudaEvent_t ev[2] = {nullptr, nullptr};
+            try {
+                cuda_check(cudaSetDevice(device), "device");
+                cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+                for (int b = 0; b < 2; ++b) {
+                    pin[b] = pinned_pool().get();
+                    cuda_check(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming), "event");
+                    if (c64)
+                        cuda_check(cudaMallocAsync(&stage[b], kChunkElems * 16, s), "cudaMallocAsync");
+                }
+                int64_t prev = -1;
+                int pslot = 0;
+                int j = 0;
+                for (int64_t i = k; i < nchunks; i += T, ++j) {
+                    const int slot = j & 1;
+                    const int64_t off = i * static_cast<int64_t>(kChunkElems);
+                    const int64_t n = std::min<int64_t>(kChunkElems, count - off);
+                    const size_t hb = static_cast<size_t>(n) * 16;
+                    if (dir == 0) {
+                        if (j >= 2)
+                            cuda_check(cudaEventSynchronize(ev[slot]), "event");
+                        std::memcpy(pin[slot], host + 2 * off, hb);
+                        if (c64) {
+                            cuda_check(cudaMemcpyAsync(stage[slot], pin[slot], hb, cudaMemcpyHostToDevice, s), "H2D");
+                            launch_check(tsk_convert(stage[slot], 0, static_cast<char*>(dev) + off * 8, 1, n, s),
+                                         "convert");
+                        } else {
+                            cuda_check(cudaMemcpyAsync(static_cast<char*>(dev) + off * 16, pin[slot], hb,
+                                                       cudaMemcpyHostToDevice, s),
+                                       "H2D");
+                        }
+                        cuda_check(cudaEventRecord(ev[slot], s), "event");
+                    } else {
+                        if (c64) {
+                            launch_check(tsk_convert(static_cast<char*>(dev) + off * 8, 1, stage[slot], 0, n, s),
+                                         "convert");
+                            cuda_check(cudaMemcpyAsync(pin[slot], stage[slot], hb, cudaMemcpyDeviceToHost, s), "D2H");
+                        } else {
+                            cuda_check(cudaMemcpyAsync(pin[slot], static_cast<char*>(dev) + off * 16, hb,
+                                                       cudaMemcpyDeviceToHost, s),
+                                       "D2H");
+                        }
+                        cuda_check(cudaEventRecord(ev[slot], s), "event");
+                        // drain the previous chunk while this one is in flight
+                        if (prev >= 0) {
+                            cuda_check(cudaEventSynchronize(ev[pslot]), "event");
+                            const int64_t po = prev * static_cast<int64_t>(kChunkElems);
+                            const int64_t pn = std::min<int64_t>(kChunkElems, count - po);
+                            std::memcpy(host + 2 * po, pin[pslot], static_cast<size_t>(pn) * 16);
+                        }
+                        prev = i;
+                        pslot = slot;
+                    }
+                }
+                if (dir == 1 && prev >= 0) {
+                    cuda_check(cudaEventSynchronize(ev[pslot]), "event");
+                    const int64_t po = prev * static_cast<int64_t>(kChunkElems);
+                    const int64_t pn = std::min<int64_t>(kChunkElems, count - po);
+                    std::memcpy(host + 2 * po, pin[pslot], static_cast<size_t>(pn) * 16);
+                }
+                cuda_check(cudaStreamSynchronize(s), "transfer sync");
+            } catch (const std::exception& e) {
+                err[k] = e.what();
+            }
+            if (s)
+                cudaStreamSynchronize(s);
+            for (int b = 0; b < 2; ++b) {
+                if (stage[b])
+                    cudaFreeAsync(stage[b], s);
+                if (pin[b])
+                    pinned_pool().put(pin[b]);
+                if (ev[b])
+                    cudaEventDestroy(ev[b]);
+            }
+            if (s) {
+                cudaStreamSynchronize(s);
+                cudaStreamDestroy(s);
+            }
+        });
+    }
+    for (auto& t : th)
+        t.join();
+    for (auto& e : err)
+        if (!e.empty())
+            fail(TS_ERR_RESOURCE, "host transfer: " + e);
+}
+
+}  // namespace
+
 void apply_host(const DeviceOperator& op, const double* v, double* y, const ts_policy* policy,
                 ts_metrics* metrics)
 {
@@ -745,7 +895,20 @@ void apply_host(const DeviceOperator& op, const double* v, double* y, const ts_p
     cuda_check(cudaEventCreate(&e0), "event");
     cuda_check(cudaEventCreate(&e1), "event");
     uint64_t ns = 0;
-    {
+    if (hbytes >= (size_t(64) << 20)) {
+        // large: chunked, multi-threaded pinned staging (no full-size complex128 copies on device)
+        AsyncBuf xw(vbytes, st), yw(vbytes, st);
+        cuda_check(cudaStreamSynchronize(st), "alloc sync");
+        host_transfer(0, op.device, const_cast<double*>(v), xw.p, op.prec != 0, count);
+        cuda_check(cudaEventRecord(e0, st), "event");
+        apply_stream(op, xw.p, yw.p, st);
+        cuda_check(cudaEventRecord(e1, st), "event");
+        cuda_check(cudaStreamSynchronize(st), "apply sync");
+        host_transfer(1, op.device, y, yw.p, op.prec != 0, count);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ns = static_cast<uint64_t>(static_cast<double>(ms) * 1e6);
+    } else {
         AsyncBuf xs(hbytes, st), ys(hbytes, st);
         AsyncBuf xw(op.prec ? vbytes : 0, st), yw(op.prec ? vbytes : 0, st);
         void* xin = op.prec ? xw.p : xs.p;
