@@ -1,6 +1,7 @@
 // Launcher-layer dispatch: the public tsk_* entry points of tsk_launch.h pick
-// the register-resident fast kernel when one exists for the pass shape and
-// fall back to the generic mixed-radix kernel otherwise.
+// the register-resident fast kernel when one exists for the pass shape, else
+// the generic mixed-radix tiled kernel, else (axis too long to stage a fiber
+// tile in shared memory) the global-memory long-axis passes.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -16,6 +17,9 @@ extern "C" int tsk_wide_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_fast_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_fast_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
 extern "C" int tsk_leaf1_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
+extern "C" int tsk_global_fwd_split(const tsk_axis* a, void* stream);
+extern "C" int tsk_global_inv_merge(const tsk_axis* a, void* stream);
+extern "C" int tsk_global_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
 
 static bool env_flag(const char* name)
 {
@@ -60,7 +64,8 @@ extern "C" int tsk_fwd_split(const tsk_axis* a, void* stream)
         if (e != -1)
             return e;
     }
-    return tsk_generic_fwd_split(a, stream);
+    const int e = tsk_generic_fwd_split(a, stream);
+    return e == -1 ? tsk_global_fwd_split(a, stream) : e;
 }
 
 extern "C" int tsk_inv_merge(const tsk_axis* a, void* stream)
@@ -73,7 +78,8 @@ extern "C" int tsk_inv_merge(const tsk_axis* a, void* stream)
         if (e != -1)
             return e;
     }
-    return tsk_generic_inv_merge(a, stream);
+    const int e = tsk_generic_inv_merge(a, stream);
+    return e == -1 ? tsk_global_inv_merge(a, stream) : e;
 }
 
 extern "C" int tsk_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream)
@@ -86,5 +92,6 @@ extern "C" int tsk_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* str
         if (e != -1)
             return e;
     }
-    return tsk_generic_leaf_pair(a, sp, stream);
+    const int e = tsk_generic_leaf_pair(a, sp, stream);
+    return e == -1 ? tsk_global_leaf_pair(a, sp, stream) : e;
 }

@@ -431,7 +431,7 @@ static int choose_w(const tsk_axis& a, bool leaf, int& W, size_t& smem)
     while (w > 1 && tile_smem(a, w, leaf) > limit)
         --w;
     if (tile_smem(a, w, leaf) > limit)
-        return (int)cudaErrorInvalidValue;  // axis too long for the generic engine
+        return -1;  // axis too long to stage a fiber: the long-axis passes take it
     W = w;
     smem = tile_smem(a, w, leaf);
     return 0;

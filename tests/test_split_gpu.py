@@ -392,3 +392,24 @@ def test_leaf_kernel_matches_previous_leaf_kernel(monkeypatch):
     ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
     op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=T.C64)
     assert rel_l2(op.apply(np.concatenate(xs)), ys) <= 1e-5
+
+
+# ---- long axes: fibers too long to stage in shared memory run the global-
+# memory passes (csrc/kernels_global.cu); the reference has no length limit
+@pytest.mark.parametrize("levels", [[5000], [4000, 3], [2, 4099], [3, 2, 3000]])
+@pytest.mark.parametrize("sym", [T.SYM_GENERAL, T.SYM_SYMMETRIC])
+def test_long_axes_vs_oracle(levels, sym):
+    g = T.Generator.random(levels, 37, 1.0, sym)
+    lags, v, y_or = _oracle_split(levels, sym, 37)
+    assert rel_l2(T.Operator.split(g).apply(v), y_or) <= 1e-12
+    op = T.Operator.split_ex(T.BlockGenerator.from_scalar(g), precision=T.C64)
+    assert rel_l2(op.apply(v), y_or) <= 1e-5
+
+
+def test_long_axis_dyadic_vs_oracle():
+    levels = [2, 3, 2500]
+    xs = _dyadic_x(levels, 41)
+    ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+    for prec, tol in ((T.C128, 1e-12), (T.C64, 1e-5)):
+        op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec)
+        assert rel_l2(op.apply(np.concatenate(xs)), ys) <= tol
