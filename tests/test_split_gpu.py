@@ -413,3 +413,53 @@ def test_long_axis_dyadic_vs_oracle():
     for prec, tol in ((T.C128, 1e-12), (T.C64, 1e-5)):
         op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec)
         assert rel_l2(op.apply(np.concatenate(xs)), ys) <= tol
+
+
+# ---- full headline size (BASELINE configs[3], 512^3 3x3 dyadic): the oracle
+# cannot run here, so parity is carried by size-independent properties of the
+# exact same kernels: the complex64 engine against the complex128 engine (a
+# different code path validated against the oracle at small sizes), linearity,
+# and the branch-partition sum identity.
+@pytest.mark.slow
+def test_c3_fullsize_c64_vs_c128_linearity_partitions():
+    import torch
+
+    levels = [512, 512, 512]
+    bg = T.BlockGenerator.dyadic(levels)
+    s = 512 ** 3
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    x1 = torch.randn(3 * s, dtype=torch.complex128, device="cuda", generator=gen)
+    op128 = T.Operator.split_ex(bg, precision=T.C128)
+    y128 = torch.empty_like(x1)
+    op128.apply_device(x1, y128)
+    torch.cuda.synchronize()
+    del op128
+    op = T.Operator.split_ex(bg, precision=T.C64)
+    x = x1.to(torch.complex64)
+    y = torch.empty_like(x)
+    op.apply_device(x, y)
+    torch.cuda.synchronize()
+    err = (torch.linalg.vector_norm(y.to(torch.complex128) - y128) / torch.linalg.vector_norm(y128)).item()
+    assert err <= 1e-5, err  # measured ~3e-7 (SURVEY.md §8(d) expectation)
+    # linearity: A(x + 2 x2) = A x + 2 A x2 (complex64 rounding only)
+    x2 = torch.randn(3 * s, dtype=torch.complex64, device="cuda", generator=gen)
+    y2 = torch.empty_like(x)
+    y3 = torch.empty_like(x)
+    op.apply_device(x2, y2)
+    op.apply_device(x + 2 * x2, y3)
+    torch.cuda.synchronize()
+    lin = (torch.linalg.vector_norm(y3 - (y + 2 * y2)) / torch.linalg.vector_norm(y3)).item()
+    assert lin <= 1e-5, lin
+    del y2, y3, x2
+    # the 8 single-branch partitions (one leaf each) sum to the whole product
+    acc = torch.zeros_like(y)
+    part = torch.empty_like(y)
+    for p in range(8):
+        opp = T.Operator.split_ex(bg, precision=T.C64, part=p, nparts=8)
+        opp.apply_device(x, part)
+        acc += part
+        del opp
+    torch.cuda.synchronize()
+    pe = (torch.linalg.vector_norm(acc - y) / torch.linalg.vector_norm(y)).item()
+    assert pe <= 1e-5, pe
+    print(f"C3 full size: c64 vs c128 rel-L2 {err:.2e}, linearity {lin:.2e}, partition sum {pe:.2e}")
