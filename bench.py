@@ -337,7 +337,7 @@ def run_b200(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = reference_sample(args, cfg, reps=1, warm=0)
+        cpu = reference_sample(args, cfg)
 
     peak_mem = torch.cuda.max_memory_allocated(dev)
     if rank == 0:
@@ -394,73 +394,96 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
-def reference_sample(args, cfg, reps=1, warm=0):
-    """Time the UNMODIFIED reference (oracle/_ref) on host cores on a bounded
-    sample of the workload and extrapolate with the reference's own C_split
-    cost model (ts_predict)."""
-    import numpy as np
+class RefSampler:
+    """The UNMODIFIED reference (oracle/_ref) on host cores, on a bounded sample
+    of the workload (same config, levels shrunk to sample_n per axis), built
+    once; one() runs one sample MVM. Times are extrapolated to the full size
+    with the reference's own C_split cost model (ts_predict)."""
 
-    import oracle
+    def __init__(self, cfg, sample_n):
+        import numpy as np
 
-    levels, kind, _, _, seed, _ = cfg
-    sample_n = int(os.environ.get("TS_REF_SAMPLE_N", "64"))
-    d = len(levels)
-    slv = [sample_n] * d
-    ncores = os.cpu_count() or 1
+        import oracle
+
+        levels, kind, _, _, seed, _ = cfg
+        self.levels, self.kind, self.n = levels, kind, sample_n
+        d = len(levels)
+        slv = [sample_n] * d
+        self.ncores = os.cpu_count() or 1
+        self.R = R = oracle.RefLib()
+        O = oracle.Oracle()
+        s = math.prod(slv)
+        self.ops = []
+        if kind == "dyadic":
+            x = O.random_vector([3] + slv, seed, 0.5)
+            self.xs = [x[i * s:(i + 1) * s] for i in range(3)]
+            for i in range(3):
+                for j in range(i, 3):
+                    lags = O.dyadic_lags(slv, i, j)
+                    g = R.generator(slv, lags, oracle.SYM_SYMMETRIC if i == j else oracle.SYM_GENERAL)
+                    self.ops.append((i, j, R.split(g)))
+                    R.destroy_gen(g)
+        else:
+            g = R.generator(slv, seed=5, symmetry=0, variance=0.5)
+            self.xs = R.random_vector(slv, seed, 0.5)
+            self.ops.append((0, 0, R.split(g)))
+            R.destroy_gen(g)
+        self.s = s
+        c_full = O.predict(d, float(levels[0]))["c_split"]
+        c_samp = O.predict(d, float(sample_n))["c_split"]
+        self.scale = c_full / c_samp
+
+    def one(self):
+        import numpy as np
+
+        R, nc = self.R, self.ncores
+        t0 = time.perf_counter()
+        if self.kind == "dyadic":
+            ys = [np.zeros(self.s, np.complex128) for _ in range(3)]
+            for i, j, op in self.ops:
+                ys[i] += R.apply(op, self.xs[j], parallel=nc)
+                if i != j:
+                    ys[j] += R.apply(op, self.xs[i], parallel=nc)
+        else:
+            R.apply(self.ops[0][2], self.xs, parallel=nc)
+        return time.perf_counter() - t0
+
+    def close(self):
+        for _, _, op in self.ops:
+            self.R.destroy_op(op)
+        self.ops = []
+
+    def describe(self, t, reps):
+        d = len(self.levels)
+        what = ("3x3 dyadic (9 scalar reference applies, G_ii symmetric, G_ij general)"
+                if self.kind == "dyadic" else "scalar")
+        return {
+            "value": 1.0 / (t * self.scale), "unit": "MVM/s", "cores": self.ncores, "kind": "reference",
+            "sample": f"{what} MVM at {self.n}^{d}, c128 (the reference's only precision), "
+                      f"TS_POLICY_PARALLEL task_budget={self.ncores}; median {t:.3f} s over {reps} rep(s), "
+                      f"extrapolated x{self.scale:.1f} to {self.levels[0]}^{d} by the reference's C_split model",
+            "sample_seconds": t,
+            "fft": "reference engine + substitute FFT (FFTW-API shim, FFTW3 absent)",
+        }
+
+
+def ref_sample_n():
+    return int(os.environ.get("TS_REF_SAMPLE_N", "128"))
+
+
+def reference_sample(args, cfg, budget_s=12.0):
+    """cpu_baseline: repeat the sample MVM for about budget_s seconds of CPU work."""
     try:
-        R = oracle.RefLib()
+        smp = RefSampler(cfg, ref_sample_n())
     except Exception as e:  # reference build absent
         return {"unavailable": f"oracle/_ref not built: {e}"}
-    O = oracle.Oracle()
-    s = math.prod(slv)
-    ops = []
-    if kind == "dyadic":
-        x = O.random_vector([3] + slv, seed, 0.5)
-        xs = [x[i * s:(i + 1) * s] for i in range(3)]
-        for i in range(3):
-            for j in range(i, 3):
-                lags = O.dyadic_lags(slv, i, j)
-                g = R.generator(slv, lags, oracle.SYM_SYMMETRIC if i == j else oracle.SYM_GENERAL)
-                ops.append((i, j, R.split(g)))
-                R.destroy_gen(g)
-
-        def one():
-            ys = [np.zeros(s, np.complex128) for _ in range(3)]
-            for i, j, op in ops:
-                ys[i] += R.apply(op, xs[j], parallel=ncores)
-                if i != j:
-                    ys[j] += R.apply(op, xs[i], parallel=ncores)
-            return ys
-    else:
-        g = R.generator(slv, seed=5, symmetry=0, variance=0.5)
-        xs = R.random_vector(slv, seed, 0.5)
-        op = R.split(g)
-        ops.append((0, 0, op))
-
-        def one():
-            return R.apply(op, xs, parallel=ncores)
-    for _ in range(warm):
-        one()
-    ts = []
-    for _ in range(max(1, reps)):
-        t0 = time.perf_counter()
-        one()
-        ts.append(time.perf_counter() - t0)
-    for _, _, op in ops:
-        R.destroy_op(op)
-    t = statistics.median(ts)
-    c_full = O.predict(d, float(levels[0]))["c_split"]
-    c_samp = O.predict(d, float(sample_n))["c_split"]
-    scale = c_full / c_samp
-    return {
-        "value": 1.0 / (t * scale), "unit": "MVM/s", "cores": ncores, "kind": "reference",
-        "sample": f"{'3x3 dyadic (9 scalar reference applies, G_ii symmetric, G_ij general)' if kind == 'dyadic' else 'scalar'} "
-                  f"MVM at {sample_n}^{d}, c128 (the reference's only precision), "
-                  f"TS_POLICY_PARALLEL task_budget={ncores}; median {t:.3f} s over {len(ts)} rep(s), "
-                  f"extrapolated x{scale:.1f} to {levels[0]}^{d} by the reference's C_split model",
-        "sample_seconds": t,
-        "fft": "reference engine + substitute FFT (FFTW-API shim, FFTW3 absent)",
-    }
+    try:
+        ts = [smp.one()]
+        reps = max(1, min(20, int(budget_s / max(ts[0], 1e-3))))
+        ts += [smp.one() for _ in range(reps - 1)]
+        return smp.describe(statistics.median(ts), len(ts))
+    finally:
+        smp.close()
 
 
 def run_reference(args):
@@ -470,19 +493,20 @@ def run_reference(args):
     cfg = CONFIGS[args.config]
     levels, kind, prec, _, _, cidx = cfg
     t0 = time.perf_counter()
+    try:
+        smp = RefSampler(cfg, ref_sample_n())
+    except Exception as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
+        return
     per = []
-    base = None
     for i in range(args.warmup + args.steps):
-        r = reference_sample(args, cfg)
-        if "unavailable" in r:
-            print(json.dumps({"impl": "reference", "unavailable": r["unavailable"]}))
-            return
+        t = smp.one()
         if i >= args.warmup:
-            per.append(1.0 / r["value"])
-            base = r
+            per.append(t * smp.scale)
+    smp.close()
+    base = smp.describe(statistics.median(per) / smp.scale, len(per))
     t_step = statistics.mean(per)
     value = 1.0 / t_step
-    base = dict(base)
     base["value"] = value
     line = {
         "metric": METRIC, "impl": "reference", "value": value, "unit": "MVM/s",
