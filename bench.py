@@ -2,7 +2,7 @@
 """Benchmark: split-FFT block-Toeplitz MVM/s on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config c3|c2|c4|c1] [--no-e2e] [--no-cpu-baseline] [--embed-baseline]
+                    [--config c3|c3full|c2|c4|c1] [--no-e2e] [--no-cpu-baseline] [--embed-baseline]
 
 Default workload (N=1): BASELINE.json configs[3] — d=3, 512^3 grid, 3x3 dyadic
 Green kernel (configs[1] definition), complex64, mirror-compressed spectra,
@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     # name: (levels, kind, precision, storage, x seed, BASELINE configs index)
     "c3": ([512, 512, 512], "dyadic", "c64", "auto", 4, 3),
+    "c3full": ([512, 512, 512], "dyadic", "c64", "full", 4, 3),  # full 6-unique spectra
     "c2": ([256, 256, 256], "dyadic", "c64", "auto", 3, 2),
     "c1": ([64, 64, 64], "dyadic", "c64", "full", 2, 1),
     "c4": ([64, 64, 64, 64], "scalar", "c64", "full", 6, 4),
