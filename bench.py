@@ -336,6 +336,15 @@ def run_b200(args):
             del ya
         del xp, yp
 
+    emb = None
+    if args.embed_baseline and kind == "dyadic" and world == 1:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import embed_baseline
+
+        op.apply_device(x, y, stream)
+        torch.cuda.synchronize()
+        emb = embed_baseline.run(levels, x, y)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = reference_sample(args, cfg)
@@ -384,6 +393,7 @@ def run_b200(args):
                                 for k, v in fam.items()},
             "gpu_launches": int(info["launches"]) * args.steps,
             "e2e": e2e,
+            "embed_baseline": emb,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "peak_device_bytes": int(peak_mem),
@@ -533,6 +543,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-abi-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--embed-baseline", action="store_true",
+                    help="also time the full-embedding MVM with cuFFT (dyadic configs; ~120 GB)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("note: the timing rules ask for >= 3 warm-up steps", file=sys.stderr)

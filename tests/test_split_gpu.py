@@ -463,3 +463,28 @@ def test_c3_fullsize_c64_vs_c128_linearity_partitions():
     pe = (torch.linalg.vector_norm(acc - y) / torch.linalg.vector_norm(y)).item()
     assert pe <= 1e-5, pe
     print(f"C3 full size: c64 vs c128 rel-L2 {err:.2e}, linearity {lin:.2e}, partition sum {pe:.2e}")
+
+
+@pytest.mark.slow
+def test_c3_fullsize_vs_cufft_embedding():
+    # an independent full-size implementation: the (2n)^3 circulant embedding
+    # with cuFFT (tools/embed_baseline.py, the dyadic formula evaluated in
+    # torch); ~106 GB of device memory at 512^3
+    import sys
+
+    import torch
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import embed_baseline
+
+    levels = [512, 512, 512]
+    s = 512 ** 3
+    op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=T.C64)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn(3 * s, dtype=torch.complex64, device="cuda", generator=gen)
+    y = torch.empty_like(x)
+    op.apply_device(x, y)
+    torch.cuda.synchronize()
+    del op
+    r = embed_baseline.run(levels, x, y, steps=1, warmup=0)
+    assert r["rel_l2_vs_split_engine"] <= 1e-5, r
