@@ -92,6 +92,13 @@ ts_status ts_operator_create_split_ex(const ts_block_generator* g, const ts_spli
 ts_status ts_operator_apply_device(const ts_operator* op, const void* x, void* y, void* stream,
                                    ts_metrics* metrics);
 
+/* nrhs right-hand sides in one call (an iterative solver's block of vectors):
+ * x and y hold nrhs vectors back to back, each laid out as for
+ * ts_operator_apply_device; same stream semantics. Counters in metrics are
+ * summed over the vectors. */
+ts_status ts_operator_apply_batch_device(const ts_operator* op, const void* x, void* y, int64_t nrhs,
+                                         void* stream, ts_metrics* metrics);
+
 typedef struct ts_operator_info {
     int32_t d;
     int32_t m;          /* vector components / block arity */

@@ -42,7 +42,7 @@ REFERENCE_SYMBOLS = [
 EXTENSION_SYMBOLS = [
     "ts_block_generator_create", "ts_block_generator_dyadic", "ts_block_generator_from_scalar",
     "ts_block_generator_components", "ts_block_generator_destroy", "ts_split_options_default",
-    "ts_operator_create_split_ex", "ts_operator_apply_device", "ts_operator_get_info",
+    "ts_operator_create_split_ex", "ts_operator_apply_device", "ts_operator_apply_batch_device", "ts_operator_get_info",
     "ts_device_count", "ts_operator_profile_device", "ts_generator_get_lags",
 ]
 LAUNCHER_SYMBOLS = [
@@ -144,6 +144,7 @@ def _load():
     L.ts_split_options_default.argtypes = [C.POINTER(TsSplitOptions)]
     L.ts_operator_create_split_ex.argtypes = [_vp, C.POINTER(TsSplitOptions), C.POINTER(_vp)]
     L.ts_operator_apply_device.argtypes = [_vp, _vp, _vp, _vp, C.POINTER(TsMetrics)]
+    L.ts_operator_apply_batch_device.argtypes = [_vp, _vp, _vp, C.c_int64, _vp, C.POINTER(TsMetrics)]
     L.ts_operator_get_info.argtypes = [_vp, C.POINTER(TsOperatorInfo)]
     L.ts_device_count.restype = C.c_int32
     L.ts_operator_profile_device.argtypes = [_vp, _vp, _vp, _vp, C.POINTER(TsLaunchRecord),
@@ -394,6 +395,18 @@ class Operator:
         _ok(lib.ts_operator_apply_device(self._h, C.c_void_p(x.data_ptr()),
                                          C.c_void_p(y.data_ptr()),
                                          C.c_void_p(stream.cuda_stream), C.byref(m)))
+        return m.as_dict() if metrics else None
+
+    def apply_batch_device(self, x, y, nrhs, stream=None, metrics=False):
+        """nrhs vectors back to back in x (and y), each as for apply_device."""
+        import torch
+
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device)
+        m = TsMetrics()
+        _ok(lib.ts_operator_apply_batch_device(self._h, C.c_void_p(x.data_ptr()),
+                                               C.c_void_p(y.data_ptr()), int(nrhs),
+                                               C.c_void_p(stream.cuda_stream), C.byref(m)))
         return m.as_dict() if metrics else None
 
     def profile_device(self, x, y, stream=None):

@@ -370,6 +370,15 @@ ts_status ts_operator_apply_device(const ts_operator* op, const void* x, void* y
     });
 }
 
+ts_status ts_operator_apply_batch_device(const ts_operator* op, const void* x, void* y, int64_t nrhs,
+                                         void* stream, ts_metrics* metrics)
+{
+    return guarded([&] {
+        need(op != nullptr);
+        apply_batch_device(*op->h.dev, x, y, nrhs, stream, metrics);
+    });
+}
+
 ts_status ts_operator_get_info(const ts_operator* op, ts_operator_info* out)
 {
     return guarded([&] {

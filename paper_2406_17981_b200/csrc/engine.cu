@@ -726,6 +726,32 @@ void apply_device(const DeviceOperator& op, const void* x, void* y, void* stream
         fill_counters(op, metrics);
 }
 
+void apply_batch_device(const DeviceOperator& op, const void* x, void* y, int64_t nrhs, void* stream,
+                        ts_metrics* metrics)
+{
+    if (!x || !y)
+        fail(TS_ERR_INVALID_ARGUMENT, "null argument");
+    if (nrhs < 1)
+        fail(TS_ERR_INVALID_ARGUMENT, "nrhs must be >= 1");
+    const size_t vb = static_cast<size_t>(op.s) * op.m * op.es();
+    const char* xb = static_cast<const char*>(x);
+    char* yb = static_cast<char*>(y);
+    if (xb < yb + vb * nrhs && yb < xb + vb * nrhs)
+        fail(TS_ERR_INVALID_ARGUMENT, "x and y must not alias");
+    DeviceGuard guard(op.device);
+    for (int64_t r = 0; r < nrhs; ++r)
+        apply_stream(op, xb + vb * r, yb + vb * r, static_cast<cudaStream_t>(stream));
+    cuda_check(cudaGetLastError(), "apply batch");
+    if (metrics) {
+        fill_counters(op, metrics);
+        const uint64_t k = static_cast<uint64_t>(nrhs);
+        metrics->fft_forward *= k;
+        metrics->fft_inverse *= k;
+        metrics->diag_mults *= k;
+        metrics->phase_mults *= k;
+    }
+}
+
 
 // ---- host <-> device transfer of the reference ABI's interleaved complex128
 // buffers. Caller memory is pageable, so a single cudaMemcpy runs at the

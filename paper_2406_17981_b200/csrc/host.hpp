@@ -98,6 +98,8 @@ void apply_host(const DeviceOperator& op, const double* v, double* y, const ts_p
                 ts_metrics* metrics);
 void apply_device(const DeviceOperator& op, const void* x, void* y, void* stream,
                   ts_metrics* metrics);
+void apply_batch_device(const DeviceOperator& op, const void* x, void* y, int64_t nrhs, void* stream,
+                        ts_metrics* metrics);
 std::vector<ts_launch_record> profile_device(const DeviceOperator& op, const void* x, void* y,
                                              void* stream);
 const Shape& operator_levels(const DeviceOperator& op);

@@ -488,3 +488,23 @@ def test_c3_fullsize_vs_cufft_embedding():
     del op
     r = embed_baseline.run(levels, x, y, steps=1, warmup=0)
     assert r["rel_l2_vs_split_engine"] <= 1e-5, r
+
+
+def test_batch_device_apply_matches_single_applies():
+    import torch
+
+    levels = [8, 16, 64]
+    bg = T.BlockGenerator.dyadic(levels)
+    op = T.Operator.split_ex(bg, precision=T.C64)
+    n = 3 * int(np.prod(levels))
+    x = torch.randn(4 * n, dtype=torch.complex64, device="cuda")
+    y = torch.empty_like(x)
+    mb = op.apply_batch_device(x, y, 4, metrics=True)
+    ys = torch.empty_like(x)
+    for r in range(4):
+        m1 = op.apply_device(x[r * n:(r + 1) * n], ys[r * n:(r + 1) * n], metrics=True)
+    torch.cuda.synchronize()
+    assert torch.equal(y, ys)
+    assert mb["fft_forward"] == 4 * m1["fft_forward"] and mb["diag_mults"] == 4 * m1["diag_mults"]
+    with pytest.raises(T.TsError):
+        op.apply_batch_device(x, x, 4)  # aliasing
