@@ -450,20 +450,57 @@ class RefSampler:
         c_samp = O.predict(d, float(sample_n))["c_split"]
         self.scale = c_full / c_samp
 
-    def one(self):
+    def one(self, parallel=None, ops=None):
         import numpy as np
 
-        R, nc = self.R, self.ncores
+        R = self.R
+        nc = self.ncores if parallel is None else parallel
+        if ops is None:
+            ops = self.ops
         t0 = time.perf_counter()
         if self.kind == "dyadic":
             ys = [np.zeros(self.s, np.complex128) for _ in range(3)]
-            for i, j, op in self.ops:
+            for i, j, op in ops:
                 ys[i] += R.apply(op, self.xs[j], parallel=nc)
                 if i != j:
                     ys[j] += R.apply(op, self.xs[i], parallel=nc)
         else:
-            R.apply(self.ops[0][2], self.xs, parallel=nc)
+            R.apply(ops[0][2], self.xs, parallel=nc)
         return time.perf_counter() - t0
+
+    def extras(self):
+        """SURVEY.md §8(d) companions at the sample size: the same MVM with the
+        LAZY policy (1 core) and with the reference's embedding engine (its
+        CPU full-embedding path), each extrapolated with its own cost model."""
+        import oracle
+
+        out = {}
+        t_lazy = self.one(parallel=0)
+        out["lazy_1core"] = {"value": 1.0 / (t_lazy * self.scale), "sample_seconds": t_lazy}
+        O = oracle.Oracle()
+        d = len(self.levels)
+        slv = [self.n] * d
+        emb = []
+        try:
+            if self.kind == "dyadic":
+                for i in range(3):
+                    for j in range(i, 3):
+                        g = self.R.generator(slv, O.dyadic_lags(slv, i, j), oracle.SYM_GENERAL)
+                        emb.append((i, j, self.R.embed(g)))
+                        self.R.destroy_gen(g)
+            else:
+                g = self.R.generator(slv, seed=5, symmetry=0, variance=0.5)
+                emb.append((0, 0, self.R.embed(g)))
+                self.R.destroy_gen(g)
+            t_emb = self.one(ops=emb)
+            ce = O.predict(d, float(self.levels[0]))["c_embed"] / O.predict(d, float(self.n))["c_embed"]
+            out["embed_engine"] = {"value": 1.0 / (t_emb * ce), "sample_seconds": t_emb,
+                                   "note": "reference CPU full-embedding engine, same composition, "
+                                           f"extrapolated x{ce:.1f} by its C_embed model"}
+        finally:
+            for _, _, op in emb:
+                self.R.destroy_op(op)
+        return out
 
     def close(self):
         for _, _, op in self.ops:
@@ -498,7 +535,12 @@ def reference_sample(args, cfg, budget_s=12.0):
         ts = [smp.one()]
         reps = max(1, min(20, int(budget_s / max(ts[0], 1e-3))))
         ts += [smp.one() for _ in range(reps - 1)]
-        return smp.describe(statistics.median(ts), len(ts))
+        out = smp.describe(statistics.median(ts), len(ts))
+        try:
+            out.update(smp.extras())
+        except Exception as e:  # companions are informational
+            out["extras_error"] = str(e)
+        return out
     finally:
         smp.close()
 
