@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 for (int m = 0; m < R; ++m) {
                     const bool mirm = 2 * m >= R;
                     const T2* sp_ = mirm ? sB - TF * m : sA + TF * m;
+                    (void)sp_;  // unused with full storage
                     T2 acc;
                     sfor<0, M>([&](auto CC) {
                         constexpr int cc = decltype(CC)::value;

@@ -119,7 +119,7 @@ __device__ __forceinline__ void fft_col(typename cx<T>::t (&v)[R], typename cx<T
 // ---- K1 / K3 ------------------------------------------------------------------
 
 template <typename T, int N, int R, int W, int MODE>
-__global__ void __launch_bounds__(N / R * W, (N / R * W) < 512 ? 512 / (N / R * W) : 1) k_wide(tsk_axis p)
+__global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512 ? 512 / (N / R * W) : 1) k_wide(tsk_axis p)
 {
     using T2 = typename cx<T>::t;
     using T4 = typename tw4<T>::t;
