@@ -43,13 +43,13 @@ def _newest(paths):
     return max((os.path.getmtime(p) for p in paths), default=0.0)
 
 
-def _compile(src: str, force: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+def _compile(src: str, force: bool, obj_dir: str = OBJ, extra=()) -> str:
+    obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(
             os.path.getmtime(src), _newest(_headers())):
         return obj
     if src.endswith(".cu"):
-        cmd = [NVCC] + CU_FLAGS + ["-c", src, "-o", obj]
+        cmd = [NVCC] + CU_FLAGS + list(extra) + ["-c", src, "-o", obj]
     else:
         cmd = ["g++"] + CXX_FLAGS + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -60,19 +60,26 @@ def _compile(src: str, force: bool) -> str:
     return obj
 
 
-def build(force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, variant: str = "", extra=()) -> str:
+    """variant: name of an A/B build (objects in build/<variant>/, library
+    ab/libtoesplit_<variant>.so, compiled with the extra nvcc flags)."""
+    obj_dir = os.path.join(OBJ, variant) if variant else OBJ
+    lib = os.path.join(ROOT, "ab", f"libtoesplit_{variant}.so") if variant else LIB
+    os.makedirs(obj_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force), srcs))
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < _newest(objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + [
+        objs = list(ex.map(lambda s: _compile(s, force, obj_dir, extra), srcs))
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < _newest(objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + [
             "-Xlinker", "-soname=libtoesplit.so.1", "-Xlinker", "-Bsymbolic",
             "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map"),
             "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    if variant:
+        return lib
     link = os.path.join(HERE, "libtoesplit.so")
     if os.path.islink(link) or os.path.exists(link):
         os.remove(link)
@@ -81,4 +88,11 @@ def build(force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv))
+    # python build.py [--force] [--variant NAME -DFLAG ...]
+    args = sys.argv[1:]
+    if "--variant" in args:
+        i = args.index("--variant")
+        print(build(force="--force" in args, variant=args[i + 1],
+                    extra=[a for a in args[i + 2:] if a != "--force"]))
+    else:
+        print(build(force="--force" in args))

@@ -29,17 +29,35 @@ using wide::Dft;
 using wide::Plan;
 using wide::Tw;
 
-__device__ __forceinline__ int orbit_members(int64_t n, int odd, int64_t s, int64_t& partner)
+// Members of the mirror orbit of stored index s along an axis of length n
+// (1 or 2) and the partner index; 32-bit (every axis length fits).
+__device__ __forceinline__ int orbit_members(int n, int odd, int s, int& partner)
 {
-    const int64_t kp = odd ? n - 1 - s : n - s;
+    const int kp = odd ? n - 1 - s : n - s;
     partner = kp;
-    if (kp >= 0 && kp < n && kp != s) {
-        bool m;
-        if (mirror_src(n, odd, kp, m) == s && m)
-            return 2;
-    }
-    return 1;
+    // kp mirrors back onto s (ref kernel.cpp:25-37) iff it lies past the
+    // stored half: odd parity stores [0, (n+1)/2), even [0, n/2]
+    const bool mirrored = odd ? kp >= (n + 1) / 2 : kp > n / 2;
+    return kp < n && kp != s && mirrored ? 2 : 1;
 }
+
+// n / d for n < 2^31 by a multiply-high (divisor fixed for the launch)
+struct FastDiv {
+    uint32_t d, mul, shift;
+    __device__ __forceinline__ explicit FastDiv(uint32_t dv) : d(dv), mul(0), shift(0)
+    {
+        if (dv > 1) {
+            uint32_t l = 32 - __clz(dv - 1);  // ceil(log2 d)
+            const uint32_t pw = 31 + l;
+            mul = (uint32_t)(((1ull << pw) + dv - 1) / dv);
+            shift = pw - 32;
+        }
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const
+    {
+        return d > 1 ? __umulhi(n, mul) >> shift : n;
+    }
+};
 
 __device__ __forceinline__ void cp_async_bytes8(void* smem, const void* gmem)
 {
@@ -207,6 +225,10 @@ constexpr int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }
 template <int N, int R, int M>
 constexpr int leaf1_g()
 {
+#ifdef LEAF_EXP_G
+    if (N == 512 && M == 3)
+        return LEAF_EXP_G;
+#endif
     return 128 / gcd_i(128, 4 * M * (N / R));
 }
 
@@ -288,6 +310,15 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     int64_t rest = 1;
     for (int a = 0; a < A1; ++a)
         rest *= sp.levels[a];
+    // per-axis masks of the unique components that are skew along the axis
+    auto axis_mask = [&](int a) {
+        uint32_t mk = 0;
+        for (int uu = 0; uu < U; ++uu)
+            mk |= ((sp.skew_mask[uu] >> a) & 1u) << uu;
+        return mk;
+    };
+    const uint32_t mask1 = A1 >= 0 ? axis_mask(A1) : 0u, mask2 = A2 >= 0 ? axis_mask(A2) : 0u;
+    const FastDiv div2((uint32_t)st2), div1((uint32_t)st1);
     // compressed: one unit = one mirror orbit; full storage: 4 consecutive fibers
     const int64_t units = CMP ? rest * st1 * st2 : (p.outer + 3) / 4;
     const T2* src = static_cast<const T2*>(p.src0);
@@ -313,22 +344,22 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 g = p.outer - 1;
             off0 = off1 = g * N;
         } else {
-            const uint32_t u32 = (uint32_t)u, st2u = (uint32_t)st2, st1u = (uint32_t)st1;
-            const uint32_t q2 = u32 / st2u, q1 = q2 / st1u;
-            const int64_t s2 = u32 - q2 * st2u, s1 = q2 - q1 * st1u, r = q1;
-            int64_t p1 = 0, p2 = 0;
-            const int c1 = A1 >= 0 ? orbit_members(n1, (bits >> A1) & 1u, s1, p1) : 1;
-            const int c2 = A2 >= 0 ? orbit_members(n2, (bits >> A2) & 1u, s2, p2) : 1;
+            // units < 2^31 (stored elements per component fit int32 here)
+            const uint32_t u32 = (uint32_t)u;
+            const uint32_t q2 = div2.div(u32), q1 = div1.div(q2);
+            const int s2 = (int)(u32 - q2 * (uint32_t)st2), s1 = (int)(q2 - q1 * (uint32_t)st1);
+            const int64_t r = q1;
+            int p1 = 0, p2 = 0;
+            const int c1 = A1 >= 0 ? orbit_members((int)n1, (bits >> A1) & 1u, s1, p1) : 1;
+            const int c2 = A2 >= 0 ? orbit_members((int)n2, (bits >> A2) & 1u, s2, p2) : 1;
             valid = uvalid && f < c1 * c2;
-            const int i1 = (f % (c1 * c2)) / c2, i2 = f % c2;
+            const int i1 = c2 == 2 ? (f >> 1) & (c1 - 1) : f & (c1 - 1), i2 = f & (c2 - 1);
             const int64_t kk1 = A1 < 0 ? 0 : (i1 ? p1 : s1);
             const int64_t kk2 = A2 < 0 ? 0 : (i2 ? p2 : s2);
-            for (int uu = 0; uu < U; ++uu) {
-                if (A1 >= 0 && i1)
-                    neg ^= ((sp.skew_mask[uu] >> A1) & 1u) << uu;
-                if (A2 >= 0 && i2)
-                    neg ^= ((sp.skew_mask[uu] >> A2) & 1u) << uu;
-            }
+            if (i1)
+                neg ^= mask1;
+            if (i2)
+                neg ^= mask2;
             int64_t rsrc = 0, rstr = 1, gr = r, rfull = 0, rmul = 1;
             for (int a = A1 - 1; a >= 0; --a) {
                 const int64_t na = sp.levels[a];
@@ -357,12 +388,19 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 return;
             const int L = beta ? N / 2 : N / 2 + 1;
             const T2* rowp = spec + sp.branch_base[beta] + (beta ? off1 : off0);
-            for (int e = lt; e < UM * L; e += UT) {
-                const int uu = e / L, kk = e - uu * L;
-                if constexpr (sizeof(T2) == 8)
-                    cp_async_bytes8(stg + uu * LROW + kk, rowp + uu * sp.block_elems[beta] + kk);
-                else
-                    cp_async_bytes16(stg + uu * LROW + kk, rowp + uu * sp.block_elems[beta] + kk);
+            const int64_t be = sp.block_elems[beta];
+#pragma unroll
+            for (int uu = 0; uu < UM; ++uu) {
+#pragma unroll
+                for (int k0 = 0; k0 < LROW; k0 += UT) {
+                    const int kk = k0 + lt;
+                    if (kk < L) {
+                        if constexpr (sizeof(T2) == 8)
+                            cp_async_bytes8(stg + uu * LROW + kk, rowp + uu * be + kk);
+                        else
+                            cp_async_bytes16(stg + uu * LROW + kk, rowp + uu * be + kk);
+                    }
+                }
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
@@ -387,7 +425,11 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
             fft_one<T, N, R, false>(v, buf, tw, t);
 
             // ---- spectra multiply y_c = sum_c' T_{c c'} x_c' (components meet in smem)
+#ifdef LEAF_EXP_NOMIX
+            if (false) {
+#else
             if (M > 1) {
+#endif
 #pragma unroll
                 for (int m = 0; m < R; ++m)
                     buf[Pad<N, R>::rd(t, m)] = v[m];
@@ -420,16 +462,31 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                         else
                             ng = neg1;
                         T2 s_;
+#ifdef LEAF_EXP_NOSPEC
+                        if constexpr (CMP)
+                            s_ = flip_bits<T>(make_c<T>((T)(uu + 1), (T)m), (ng >> uu) & 1u);
+#elif defined(LEAF_EXP_NOFLIP)
+                        if constexpr (CMP)
+                            s_ = sp_[uu * LROW];
+#else
                         if constexpr (CMP)
                             s_ = flip_bits<T>(sp_[uu * LROW], (ng >> uu) & 1u);
+#endif
                         else  // full storage: this fiber's own row, read once
                             s_ = ldg_c(spec + sp.branch_base[beta] + (beta ? off1 : off0) +
                                        uu * sp.block_elems[beta] + t + TF * m);
+#ifdef LEAF_EXP_NOMIX
+                        const T2 xv = v[m];
+#else
                         const T2 xv = cc == C ? v[m] : fbufs[(f * M + cc) * NP + Pad<N, R>::rd(t, m)];
+#endif
                         acc = cmac<T>(acc, xv, s_, cc == 0);
                     });
                     v[m] = acc;
-                    if (m % 2 == 1)
+#ifndef LEAF_EXP_FENCE
+#define LEAF_EXP_FENCE 2
+#endif
+                    if (m % LEAF_EXP_FENCE == LEAF_EXP_FENCE - 1)
                         asm volatile("" ::: "memory");  // bound the loads in flight
                 }
             };
@@ -543,6 +600,8 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         for (int ax = 0; ax < sp.d - 1; ++ax)
             units *= ax >= sp.d - 3 ? stored_len(sp.levels[ax], (sp.branch_bits[0] >> ax) & 1u)
                                     : sp.levels[ax];
+        if (units >= (int64_t(1) << 31))
+            return -1;  // FastDiv / 32-bit orbit indices
     } else {
         units = (a.outer + 3) / 4;
     }
