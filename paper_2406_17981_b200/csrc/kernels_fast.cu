@@ -460,11 +460,15 @@ __global__ void __launch_bounds__(N / 8 * W) k_strided(tsk_axis p)
     const bool ld0 = MODE == 0 || ue, ld1 = MODE == 1 && uo;
     const int64_t rstride = (int64_t)TF * inner;  // element stride between m and m+1
 
+    const FastDiv div_tpc((uint32_t)tiles_per_comp), div_cols((uint32_t)cols);
     auto tile_base = [&](int64_t tile) {
-        const int64_t c = tile / tiles_per_comp;
-        const int64_t r = tile - c * tiles_per_comp;
-        const int64_t o = r / cols;
-        const int64_t i0 = (r - o * cols) * W;
+        // launcher guarantees ntiles < 2^31
+        const uint32_t t32 = (uint32_t)tile;
+        const uint32_t c32 = div_tpc.div(t32);
+        const uint32_t r32 = t32 - c32 * (uint32_t)tiles_per_comp;
+        const uint32_t o32 = div_cols.div(r32);
+        const int64_t c = c32, o = o32;
+        const int64_t i0 = (int64_t)(r32 - o32 * (uint32_t)cols) * W;
         return c * p.cstride + o * (int64_t)N * inner + i0 + w + (int64_t)t * inner;
     };
     T2 nx[NIN][8];
@@ -964,6 +968,8 @@ static int launch_strided(const tsk_axis& a, cudaStream_t st)
     if (int e = prep(kern, smem, N / 8 * W, cap))
         return e;
     const int64_t ntiles = a.outer * (a.inner / W) * a.ncomp;
+    if (ntiles >= (int64_t(1) << 31))
+        return -1;  // 32-bit tile decomposition
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, cap));
     kern<<<(unsigned)grid, N / 8 * W, smem, st>>>(a);
     return (int)cudaGetLastError();

@@ -41,23 +41,6 @@ __device__ __forceinline__ int orbit_members(int n, int odd, int s, int& partner
     return kp < n && kp != s && mirrored ? 2 : 1;
 }
 
-// n / d for n < 2^31 by a multiply-high (divisor fixed for the launch)
-struct FastDiv {
-    uint32_t d, mul, shift;
-    __device__ __forceinline__ explicit FastDiv(uint32_t dv) : d(dv), mul(0), shift(0)
-    {
-        if (dv > 1) {
-            uint32_t l = 32 - __clz(dv - 1);  // ceil(log2 d)
-            const uint32_t pw = 31 + l;
-            mul = (uint32_t)(((1ull << pw) + dv - 1) / dv);
-            shift = pw - 32;
-        }
-    }
-    __device__ __forceinline__ uint32_t div(uint32_t n) const
-    {
-        return d > 1 ? __umulhi(n, mul) >> shift : n;
-    }
-};
 
 __device__ __forceinline__ void cp_async_bytes8(void* smem, const void* gmem)
 {

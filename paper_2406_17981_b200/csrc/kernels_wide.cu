@@ -162,11 +162,16 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
         }
     }
 
+    // tile -> (component, outer, column block) by multiply-high (the
+    // launcher guarantees ntiles < 2^31)
+    const FastDiv div_tpc((uint32_t)tiles_per_comp), div_cols((uint32_t)cols);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t c = tile / tiles_per_comp;
-        const int64_t r = tile - c * tiles_per_comp;
-        const int64_t o = r / cols;
-        const int64_t i0 = (r - o * cols) * W;
+        const uint32_t t32 = (uint32_t)tile;
+        const uint32_t c32 = div_tpc.div(t32);
+        const uint32_t r32 = t32 - c32 * (uint32_t)tiles_per_comp;
+        const uint32_t o32 = div_cols.div(r32);
+        const int64_t c = c32, o = o32;
+        const int64_t i0 = (int64_t)(r32 - o32 * (uint32_t)cols) * W;
         const int64_t base = c * p.cstride + o * (int64_t)N * inner + i0 + w + (int64_t)t * inner;
         T2 v[R];
         T2 ekeep[TM ? 1 : R];
@@ -289,6 +294,8 @@ static int launch(const tsk_axis& a, cudaStream_t st)
         cached_dev = dev;
     }
     const int64_t ntiles = a.outer * (a.inner / G::W) * a.ncomp;
+    if (ntiles >= (int64_t(1) << 31))
+        return -1;  // 32-bit tile decomposition
     const int64_t grid = ntiles < cap ? ntiles : cap;
     kern<<<(unsigned)(grid > 0 ? grid : 1), G::NT, smem, st>>>(a);
     return (int)cudaGetLastError();
