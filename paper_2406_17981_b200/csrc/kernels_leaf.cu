@@ -496,39 +496,51 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                     for (int m = 0; m < R; ++m)
                         ekeep[m] = v[m];
             } else {
-                // e' comes back from TMEM 32 words at a time (bounded registers)
+                // e' comes back from TMEM 32 words at a time (bounded registers);
+                // the branch conditions are resolved once, outside the element loop
                 constexpr int EPC = TM ? 32 / ((int)sizeof(T2) / 4) : R;
                 T2* yout = dst + c * p.cstride + g * N + t;
-                sfor<0, R / EPC>([&](auto C) {
-                    constexpr int c0 = decltype(C)::value * EPC;
-                    T2 e[EPC];
-                    if (both) {
-                        if constexpr (TM) {
-                            uint32_t r[32];
-                            tmem_ld32(lane_base + c0 * ((int)sizeof(T2) / 4), r);
+                auto emit = [&](auto ODD, auto BOTH) {
+                    constexpr bool odd = decltype(ODD)::value, bth = decltype(BOTH)::value;
+                    sfor<0, R / EPC>([&](auto C) {
+                        constexpr int c0 = decltype(C)::value * EPC;
+                        T2 e[EPC];
+                        if constexpr (bth) {
+                            if constexpr (TM) {
+                                uint32_t r[32];
+                                tmem_ld32(lane_base + c0 * ((int)sizeof(T2) / 4), r);
 #pragma unroll
-                            for (int i = 0; i < EPC; ++i)
-                                e[i] = Words<T2>::make(r + i * Words<T2>::W);
-                        } else {
+                                for (int i = 0; i < EPC; ++i)
+                                    e[i] = Words<T2>::make(r + i * Words<T2>::W);
+                            } else {
 #pragma unroll
-                            for (int i = 0; i < EPC; ++i)
-                                e[i] = ekeep[c0 + i];
+                                for (int i = 0; i < EPC; ++i)
+                                    e[i] = ekeep[c0 + i];
+                            }
                         }
-                    }
-                    sfor<0, EPC>([&](auto I) {
-                        constexpr int mi = c0 + decltype(I)::value;
-                        T2 a;
-                        if (beta == 1) {
-                            a = PhaseR<T, R, true>::template apply<mi>(v[mi], pts);
-                            if (both)
-                                a = fma_s<T>(e[decltype(I)::value], scale, a);
-                        } else {
-                            a = make_c<T>(v[mi].x * scale, v[mi].y * scale);
-                        }
-                        if (valid)
-                            yout[mi * TF] = a;
+                        sfor<0, EPC>([&](auto I) {
+                            constexpr int mi = c0 + decltype(I)::value;
+                            T2 a;
+                            if constexpr (odd) {
+                                a = PhaseR<T, R, true>::template apply<mi>(v[mi], pts);
+                                if constexpr (bth)
+                                    a = fma_s<T>(e[decltype(I)::value], scale, a);
+                            } else {
+                                a = make_c<T>(v[mi].x * scale, v[mi].y * scale);
+                            }
+                            if (valid)
+                                yout[mi * TF] = a;
+                        });
                     });
-                });
+                };
+                using B0 = std::false_type;
+                using B1 = std::true_type;
+                if (beta == 0)
+                    emit(B0{}, B0{});
+                else if (both)
+                    emit(B1{}, B1{});
+                else
+                    emit(B1{}, B0{});
             }
         }
     }
