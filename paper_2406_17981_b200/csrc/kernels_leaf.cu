@@ -208,10 +208,6 @@ constexpr int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }
 template <int N, int R, int M>
 constexpr int leaf1_g()
 {
-#ifdef LEAF_EXP_G
-    if (N == 512 && M == 3)
-        return LEAF_EXP_G;
-#endif
     return 128 / gcd_i(128, 4 * M * (N / R));
 }
 
@@ -314,55 +310,60 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
         const bool uvalid = u < units;
         if (!uvalid)
             u = units - 1;  // runs in lockstep (barriers), stores nothing
-        // ---- unit geometry: fiber g of orbit member f, spectra row, signs.
-        // Members past the orbit size alias a real member (loads stay in
+        // ---- unit geometry: fiber g of orbit member f, spectra row offsets,
+        // signs. Members past the orbit size alias a real member (loads stay in
         // range) and skip the store.
+        auto geometry = [&](int64_t u, bool uvalid, bool& valid, int64_t& g, int64_t& off0, int64_t& off1,
+                            uint32_t& neg) {
+            neg = 0;
+            if constexpr (!CMP) {
+                g = u * 4 + f;
+                valid = uvalid && g < p.outer;
+                if (g >= p.outer)
+                    g = p.outer - 1;
+                off0 = off1 = g * N;
+            } else {
+                // units < 2^31 (stored elements per component fit int32 here)
+                const uint32_t u32 = (uint32_t)u;
+                const uint32_t q2 = div2.div(u32), q1 = div1.div(q2);
+                const int s2 = (int)(u32 - q2 * (uint32_t)st2), s1 = (int)(q2 - q1 * (uint32_t)st1);
+                const int64_t r = q1;
+                int p1 = 0, p2 = 0;
+                const int c1 = A1 >= 0 ? orbit_members((int)n1, (bits >> A1) & 1u, s1, p1) : 1;
+                const int c2 = A2 >= 0 ? orbit_members((int)n2, (bits >> A2) & 1u, s2, p2) : 1;
+                valid = uvalid && f < c1 * c2;
+                const int i1 = c2 == 2 ? (f >> 1) & (c1 - 1) : f & (c1 - 1), i2 = f & (c2 - 1);
+                const int64_t kk1 = A1 < 0 ? 0 : (i1 ? p1 : s1);
+                const int64_t kk2 = A2 < 0 ? 0 : (i2 ? p2 : s2);
+                if (i1)
+                    neg ^= mask1;
+                if (i2)
+                    neg ^= mask2;
+                int64_t rsrc = 0, rstr = 1, gr = r, rfull = 0, rmul = 1;
+                for (int a = A1 - 1; a >= 0; --a) {
+                    const int64_t na = sp.levels[a];
+                    const int64_t ka = gr % na;
+                    gr /= na;
+                    const int odd = (bits >> a) & 1u;
+                    bool mm;
+                    rsrc += mirror_src(na, odd, ka, mm) * rstr;
+                    rstr *= stored_len(na, odd);
+                    rfull += ka * rmul;
+                    rmul *= na;
+                    if (mm)
+                        for (int uu = 0; uu < U; ++uu)
+                            neg ^= ((sp.skew_mask[uu] >> a) & 1u) << uu;
+                }
+                g = (rfull * n1 + kk1) * n2 + kk2;
+                const int64_t row = (rsrc * st1 + s1) * st2 + s2;
+                off0 = row * (N / 2 + 1);
+                off1 = row * (N / 2);
+            }
+        };
         bool valid;
         int64_t g, off0, off1;
-        uint32_t neg = 0;
-        if constexpr (!CMP) {
-            g = u * 4 + f;
-            valid = uvalid && g < p.outer;
-            if (g >= p.outer)
-                g = p.outer - 1;
-            off0 = off1 = g * N;
-        } else {
-            // units < 2^31 (stored elements per component fit int32 here)
-            const uint32_t u32 = (uint32_t)u;
-            const uint32_t q2 = div2.div(u32), q1 = div1.div(q2);
-            const int s2 = (int)(u32 - q2 * (uint32_t)st2), s1 = (int)(q2 - q1 * (uint32_t)st1);
-            const int64_t r = q1;
-            int p1 = 0, p2 = 0;
-            const int c1 = A1 >= 0 ? orbit_members((int)n1, (bits >> A1) & 1u, s1, p1) : 1;
-            const int c2 = A2 >= 0 ? orbit_members((int)n2, (bits >> A2) & 1u, s2, p2) : 1;
-            valid = uvalid && f < c1 * c2;
-            const int i1 = c2 == 2 ? (f >> 1) & (c1 - 1) : f & (c1 - 1), i2 = f & (c2 - 1);
-            const int64_t kk1 = A1 < 0 ? 0 : (i1 ? p1 : s1);
-            const int64_t kk2 = A2 < 0 ? 0 : (i2 ? p2 : s2);
-            if (i1)
-                neg ^= mask1;
-            if (i2)
-                neg ^= mask2;
-            int64_t rsrc = 0, rstr = 1, gr = r, rfull = 0, rmul = 1;
-            for (int a = A1 - 1; a >= 0; --a) {
-                const int64_t na = sp.levels[a];
-                const int64_t ka = gr % na;
-                gr /= na;
-                const int odd = (bits >> a) & 1u;
-                bool mm;
-                rsrc += mirror_src(na, odd, ka, mm) * rstr;
-                rstr *= stored_len(na, odd);
-                rfull += ka * rmul;
-                rmul *= na;
-                if (mm)
-                    for (int uu = 0; uu < U; ++uu)
-                        neg ^= ((sp.skew_mask[uu] >> a) & 1u) << uu;
-            }
-            g = (rfull * n1 + kk1) * n2 + kk2;
-            const int64_t row = (rsrc * st1 + s1) * st2 + s2;
-            off0 = row * (N / 2 + 1);
-            off1 = row * (N / 2);
-        }
+        uint32_t neg;
+        geometry(u, uvalid, valid, g, off0, off1, neg);
         // sign masks per unique component: bit uu of neg (unmirrored k) and
         // of neg ^ lastneg (mirrored k)
         const uint32_t neg0 = neg, neg1 = neg ^ lastneg;
@@ -408,11 +409,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
             fft_one<T, N, R, false>(v, buf, tw, t);
 
             // ---- spectra multiply y_c = sum_c' T_{c c'} x_c' (components meet in smem)
-#ifdef LEAF_EXP_NOMIX
-            if (false) {
-#else
             if (M > 1) {
-#endif
 #pragma unroll
                 for (int m = 0; m < R; ++m)
                     buf[Pad<N, R>::rd(t, m)] = v[m];
@@ -445,31 +442,16 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                         else
                             ng = neg1;
                         T2 s_;
-#ifdef LEAF_EXP_NOSPEC
-                        if constexpr (CMP)
-                            s_ = flip_bits<T>(make_c<T>((T)(uu + 1), (T)m), (ng >> uu) & 1u);
-#elif defined(LEAF_EXP_NOFLIP)
-                        if constexpr (CMP)
-                            s_ = sp_[uu * LROW];
-#else
                         if constexpr (CMP)
                             s_ = flip_bits<T>(sp_[uu * LROW], (ng >> uu) & 1u);
-#endif
                         else  // full storage: this fiber's own row, read once
                             s_ = ldg_c(spec + sp.branch_base[beta] + (beta ? off1 : off0) +
                                        uu * sp.block_elems[beta] + t + TF * m);
-#ifdef LEAF_EXP_NOMIX
-                        const T2 xv = v[m];
-#else
                         const T2 xv = cc == C ? v[m] : fbufs[(f * M + cc) * NP + Pad<N, R>::rd(t, m)];
-#endif
                         acc = cmac<T>(acc, xv, s_, cc == 0);
                     });
                     v[m] = acc;
-#ifndef LEAF_EXP_FENCE
-#define LEAF_EXP_FENCE 2
-#endif
-                    if (m % LEAF_EXP_FENCE == LEAF_EXP_FENCE - 1)
+                    if (m % 2 == 1)
                         asm volatile("" ::: "memory");  // bound the loads in flight
                 }
             };
