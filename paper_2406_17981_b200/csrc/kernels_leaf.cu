@@ -202,6 +202,30 @@ __device__ __forceinline__ void fft_one(typename cx<T>::t (&v)[R], typename cx<T
     }
 }
 
+// Components meet in tensor memory (MIXT): the threads of one (unit, fiber,
+// t) in the M component warps share a TMEM lane (warps q, q+4, q+8), so each
+// writes its transform to its own column block of that lane and reads the
+// others' — the exchange uses the TMEM datapath instead of the shared-memory
+// pipe, which the FFT exchanges and the spectra reads keep busy.
+#ifndef TSK_LEAF_MIXT
+#define TSK_LEAF_MIXT 1
+#endif
+// (Compressed storage only: with full storage the leaf reads each fiber's own
+// spectra from global memory and the extra registers of the TMEM chunks spill,
+// measured 3.83 -> 4.33 ms per launch at 512^3.)
+template <typename T, int R, int M, bool CMP>
+constexpr bool leaf_mixt()
+{
+    return TSK_LEAF_MIXT && CMP && M > 1 && (R * (int)sizeof(typename cx<T>::t) / 4) % 32 == 0;
+}
+// TMEM columns per CTA: e' park (+ component exchange) for NW warps
+template <typename T, int R, int M, bool CMP, int NW>
+constexpr int leaf_tcols()
+{
+    constexpr int EW = R * (int)sizeof(typename cx<T>::t) / 4;
+    return tmem_cols_pow2(EW * ((NW + 3) / 4) * (leaf_mixt<T, R, M, CMP>() ? 2 : 1));
+}
+
 // units (orbits) per CTA: warps per CTA a multiple of 4 (even split over the
 // SM sub-partitions' register files)
 constexpr int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }
@@ -258,7 +282,9 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     constexpr int EW = R * (int)sizeof(T2) / 4;
     constexpr bool TM = EW % 32 == 0;
     constexpr int NW = NT / 32 > 0 ? NT / 32 : 1;
-    constexpr int TCOLS = tmem_cols_pow2(EW * ((NW + 3) / 4));
+    constexpr int TCOLS = leaf_tcols<T, R, M, CMP, NW>();
+    constexpr bool MIXT = leaf_mixt<T, R, M, CMP>();
+    constexpr int MIXOFF = EW * ((NW + 3) / 4);  // first column of the exchange blocks
     uint32_t tbase = 0, lane_base = 0;
     if constexpr (TM) {
         tbase = tmem_alloc(&tmem_slot, TCOLS);
@@ -409,13 +435,20 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
             fft_one<T, N, R, false>(v, buf, tw, t);
 
             // ---- spectra multiply y_c = sum_c' T_{c c'} x_c' (components meet in smem)
-            if (M > 1) {
+            // lane quadrant of this warp (the exchange blocks of its partners)
+            const uint32_t quad = tbase + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16);
+            if constexpr (MIXT) {
+                tmem_park<T, R>(quad + MIXOFF + EW * c, v);
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            } else if (M > 1) {
 #pragma unroll
                 for (int m = 0; m < R; ++m)
                     buf[Pad<N, R>::rd(t, m)] = v[m];
             }
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             unit_sync();
+            if constexpr (MIXT)
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             // stored half-spectrum index: k = t + TF m below N/2, mirrored
             // (N - beta - k) from N/2 up; k = N/2 (t = 0, even) maps to itself
             auto mix = [&](auto CI) {
@@ -423,8 +456,27 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 const T2* sA = stg + t;
                 const T2* sB = stg + (N - beta - t);
                 const bool t0 = t == 0;
+                constexpr int XCH = 16 / Words<T2>::W;  // values per 16-column TMEM read
+                T2 xo[M][XCH];          // partners' values of the current chunk
 #pragma unroll
                 for (int m = 0; m < R; ++m) {
+                    if constexpr (MIXT) {
+                        if (m % XCH == 0) {
+                            constexpr int WPC = 16;  // words per chunk
+                            uint32_t r[M][16];
+#pragma unroll
+                            for (int cc = 0; cc < M; ++cc)
+                                if (cc != C)
+                                    tmem_ld16(quad + MIXOFF + EW * cc + (m / XCH) * WPC, r[cc]);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int cc = 0; cc < M; ++cc)
+                                if (cc != C)
+#pragma unroll
+                                    for (int i = 0; i < XCH; ++i)
+                                        xo[cc][i] = Words<T2>::make(r[cc] + i * Words<T2>::W);
+                        }
+                    }
                     const bool mirm = 2 * m >= R;
                     const T2* sp_ = mirm ? sB - TF * m : sA + TF * m;
                     (void)sp_;  // unused with full storage
@@ -447,7 +499,13 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                         else  // full storage: this fiber's own row, read once
                             s_ = ldg_c(spec + sp.branch_base[beta] + (beta ? off1 : off0) +
                                        uu * sp.block_elems[beta] + t + TF * m);
-                        const T2 xv = cc == C ? v[m] : fbufs[(f * M + cc) * NP + Pad<N, R>::rd(t, m)];
+                        T2 xv;
+                        if constexpr (cc == C)
+                            xv = v[m];
+                        else if constexpr (MIXT)
+                            xv = xo[cc][m % XCH];
+                        else
+                            xv = fbufs[(f * M + cc) * NP + Pad<N, R>::rd(t, m)];
                         acc = cmac<T>(acc, xv, s_, cc == 0);
                     });
                     v[m] = acc;
@@ -465,7 +523,11 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 else
                     mix(std::integral_constant<int, 2>{});
             }
+            if constexpr (MIXT)
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             unit_sync();  // staged row and mix buffers free
+            if constexpr (MIXT)
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (beta == 0 && uo)
                 stage_row(1);
             fft_one<T, N, R, true>(v, buf, tw, t);
@@ -563,7 +625,7 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         // TMEM: every resident CTA allocates its columns
         constexpr int EW = R * (int)sizeof(T2) / 4;
         constexpr int NW = NT / 32 > 0 ? NT / 32 : 1;
-        constexpr int TC = tmem_cols_pow2(EW * ((NW + 3) / 4));
+        constexpr int TC = leaf_tcols<T, R, M, CMP, NW>();
         if (EW % 32 == 0 && per_sm * TC > 512)
             per_sm = 512 / TC;
         if (getenv("TSK_DEBUG_OCC"))
