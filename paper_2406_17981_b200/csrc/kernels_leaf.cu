@@ -164,9 +164,11 @@ __device__ __forceinline__ void sfor(F&& f)
 }
 
 // One length-N transform of this thread's row pattern v[m] = x[t + TF m].
-template <typename T, int N, int R, bool INV>
+// TWT: the stage-B twiddles of this thread's two butterflies come from its
+// TMEM lane (32 columns per butterfly at twt) instead of the shared table.
+template <typename T, int N, int R, bool INV, bool TWT = false>
 __device__ __forceinline__ void fft_one(typename cx<T>::t (&v)[R], typename cx<T>::t* buf,
-                                        const typename cx<T>::t* tw, int t)
+                                        const typename cx<T>::t* tw, int t, uint32_t twt = 0)
 {
     using T2 = typename cx<T>::t;
     constexpr int TF = N / R;
@@ -189,10 +191,23 @@ __device__ __forceinline__ void fft_one(typename cx<T>::t (&v)[R], typename cx<T
         const int j = t + i * TF;
         T2 a[P2];
         a[0] = v[i];
+        if constexpr (TWT) {
+            static_assert(sizeof(T2) == 8 && P2 == 16, "TMEM twiddles: complex64, radix 16");
+            uint32_t r32[32];
+            tmem_ld32(twt + 32 * i, r32);  // waits
 #pragma unroll
-        for (int r = 1; r < P2; ++r) {
-            const Tw<T> w = wide::load_tw<T>(tw + j * (P2 - 1) + (r - 1));
-            a[r] = wide::cmul_tw<T, INV>(v[i + r * G2], w);
+            for (int r = 1; r < P2; ++r) {
+                Tw<T> w;
+                w.lo = Words<T2>::make(r32 + 2 * (r - 1));
+                w.hi = w.lo;
+                a[r] = wide::cmul_tw<T, INV>(v[i + r * G2], w);
+            }
+        } else {
+#pragma unroll
+            for (int r = 1; r < P2; ++r) {
+                const Tw<T> w = wide::load_tw<T>(tw + j * (P2 - 1) + (r - 1));
+                a[r] = wide::cmul_tw<T, INV>(v[i + r * G2], w);
+            }
         }
         Dft<T, P2, INV>::run(a);
 #pragma unroll
@@ -217,6 +232,16 @@ template <typename T, int R, int M, bool CMP>
 constexpr bool leaf_mixt()
 {
     return TSK_LEAF_MIXT && CMP && M > 1 && (R * (int)sizeof(typename cx<T>::t) / 4) % 32 == 0;
+}
+#ifndef TSK_LEAF_TWT
+#define TSK_LEAF_TWT 1
+#endif
+template <typename T, int N, int R, int M, bool CMP, int NW>
+constexpr bool leaf_twt()
+{
+    constexpr int EW = R * (int)sizeof(typename cx<T>::t) / 4;
+    return TSK_LEAF_TWT && leaf_mixt<T, R, M, CMP>() && sizeof(T) == 4 && R == 32 && N == 512 &&
+           2 * EW * ((NW + 3) / 4) + 64 <= 512;
 }
 // TMEM columns per CTA: e' park (+ component exchange) for NW warps
 template <typename T, int R, int M, bool CMP, int NW>
@@ -285,15 +310,44 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     constexpr int TCOLS = leaf_tcols<T, R, M, CMP, NW>();
     constexpr bool MIXT = leaf_mixt<T, R, M, CMP>();
     constexpr int MIXOFF = EW * ((NW + 3) / 4);  // first column of the exchange blocks
+    // stage-B twiddles in TMEM (after the exchange blocks; 64 columns)
+    constexpr bool TWT = leaf_twt<T, N, R, M, CMP, NW>();
+    constexpr int TWOFF = 2 * MIXOFF;
     uint32_t tbase = 0, lane_base = 0;
     if constexpr (TM) {
         tbase = tmem_alloc(&tmem_slot, TCOLS);
         lane_base = tbase + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16) +
                     (uint32_t)(EW * ((threadIdx.x / 32) / 4));
+        if constexpr (TWT) {
+            // the first warp of each lane quadrant writes its lanes' twiddles
+            // w_N^{r j}, j = t + i TF (the component warps of a lane share t)
+            if ((threadIdx.x / 32) / 4 == 0) {
+                const int tl = threadIdx.x % TF;
+                const uint32_t q = tbase + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16) + TWOFF;
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    uint32_t r32[32];
+#pragma unroll
+                    for (int r = 1; r < 16; ++r) {
+                        const T2 w = ldg_c(static_cast<const T2*>(p.roots) + (r * (tl + i * TF)) % N);
+                        r32[2 * (r - 1)] = __float_as_uint(w.x);
+                        r32[2 * (r - 1) + 1] = __float_as_uint(w.y);
+                    }
+                    r32[30] = r32[31] = 0u;
+                    tmem_st32(q + 32 * i, r32);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncthreads();
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
     } else {
         __syncthreads();
     }
 
+    // lane quadrant of this warp (its partners' exchange blocks, the twiddles)
+    const uint32_t quad = tbase + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16);
     const int d = sp.d;
     const int U = sp.n_unique;
     const bool ue = p.use_even, uo = p.use_odd, both = ue && uo;
@@ -432,11 +486,9 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                     constexpr int mi = decltype(I)::value;
                     v[mi] = PhaseR<T, R, false>::template apply<mi>(v[mi], pt);
                 });
-            fft_one<T, N, R, false>(v, buf, tw, t);
+            fft_one<T, N, R, false, TWT>(v, buf, tw, t, quad + TWOFF);
 
             // ---- spectra multiply y_c = sum_c' T_{c c'} x_c' (components meet in smem)
-            // lane quadrant of this warp (the exchange blocks of its partners)
-            const uint32_t quad = tbase + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16);
             if constexpr (MIXT) {
                 tmem_park<T, R>(quad + MIXOFF + EW * c, v);
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -530,7 +582,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (beta == 0 && uo)
                 stage_row(1);
-            fft_one<T, N, R, true>(v, buf, tw, t);
+            fft_one<T, N, R, true, TWT>(v, buf, tw, t, quad + TWOFF);
 
             if (beta == 0 && both) {
                 if constexpr (TM)
