@@ -241,7 +241,7 @@ constexpr bool leaf_twt()
 {
     constexpr int EW = R * (int)sizeof(typename cx<T>::t) / 4;
     return TSK_LEAF_TWT && leaf_mixt<T, R, M, CMP>() && sizeof(T) == 4 && R == 32 && N == 512 &&
-           2 * EW * ((NW + 3) / 4) + 64 <= 512;
+           2 * EW * ((NW + 3) / 4) + 128 <= 512;
 }
 // TMEM columns per CTA: e' park (+ component exchange) for NW warps
 template <typename T, int R, int M, bool CMP, int NW>
@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     // stage-B twiddles in TMEM (after the exchange blocks; 64 columns)
     constexpr bool TWT = leaf_twt<T, N, R, M, CMP, NW>();
     constexpr int TWOFF = 2 * MIXOFF;
+    constexpr int PHOFF = TWOFF + 64;  // phase table (TWT: 64 columns)
     uint32_t tbase = 0, lane_base = 0;
     if constexpr (TM) {
         tbase = tmem_alloc(&tmem_slot, TCOLS);
@@ -335,6 +336,18 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                     }
                     r32[30] = r32[31] = 0u;
                     tmem_st32(q + 32 * i, r32);
+                }
+                // split phase P_k = exp(-i pi k / N) at this lane's k = t + TF m
+#pragma unroll
+                for (int h = 0; h < R / 16; ++h) {
+                    uint32_t r32[32];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const T2 w = ldg_c(static_cast<const T2*>(p.phase) + tl + TF * (16 * h + i));
+                        r32[2 * i] = __float_as_uint(w.x);
+                        r32[2 * i + 1] = __float_as_uint(w.y);
+                    }
+                    tmem_st32(q + 64 + 32 * h, r32);
                 }
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
@@ -481,11 +494,28 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
 #pragma unroll
             for (int m = 0; m < R; ++m)
                 v[m] = xin[m * TF];
-            if (beta == 1)
-                sfor<0, R>([&](auto I) {
-                    constexpr int mi = decltype(I)::value;
-                    v[mi] = PhaseR<T, R, false>::template apply<mi>(v[mi], pt);
-                });
+            if (beta == 1) {
+                if constexpr (TWT) {
+                    // P_k from this lane's TMEM table: one complex product
+#pragma unroll
+                    for (int h = 0; h < R / 16; ++h) {
+                        uint32_t r32[32];
+                        tmem_ld32(quad + PHOFF + 32 * h, r32);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            Tw<T> w;
+                            w.lo = Words<T2>::make(r32 + 2 * i);
+                            w.hi = w.lo;
+                            v[16 * h + i] = wide::cmul_tw<T, false>(v[16 * h + i], w);
+                        }
+                    }
+                } else {
+                    sfor<0, R>([&](auto I) {
+                        constexpr int mi = decltype(I)::value;
+                        v[mi] = PhaseR<T, R, false>::template apply<mi>(v[mi], pt);
+                    });
+                }
+            }
             fft_one<T, N, R, false, TWT>(v, buf, tw, t, quad + TWOFF);
 
             // ---- spectra multiply y_c = sum_c' T_{c c'} x_c' (components meet in smem)
@@ -594,14 +624,30 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
             } else {
                 // e' comes back from TMEM 32 words at a time (bounded registers);
                 // the branch conditions are resolved once, outside the element loop
-                constexpr int EPC = TM ? 32 / ((int)sizeof(T2) / 4) : R;
+                constexpr int EPC = TWT ? 8 : TM ? 32 / ((int)sizeof(T2) / 4) : R;
                 T2* yout = dst + c * p.cstride + g * N + t;
                 auto emit = [&](auto ODD, auto BOTH) {
                     constexpr bool odd = decltype(ODD)::value, bth = decltype(BOTH)::value;
                     sfor<0, R / EPC>([&](auto C) {
                         constexpr int c0 = decltype(C)::value * EPC;
-                        T2 e[EPC];
-                        if constexpr (bth) {
+                        T2 e[EPC], ph[TWT ? EPC : 1];
+                        if constexpr (TWT && odd) {
+                            uint32_t r[16];
+                            tmem_ld16(quad + PHOFF + c0 * 2, r);
+                            if constexpr (bth) {
+                                uint32_t re[16];
+                                tmem_ld16(lane_base + c0 * 2, re);
+                                tmem_wait_ld();
+#pragma unroll
+                                for (int i = 0; i < EPC; ++i)
+                                    e[i] = Words<T2>::make(re + 2 * i);
+                            } else {
+                                tmem_wait_ld();
+                            }
+#pragma unroll
+                            for (int i = 0; i < EPC; ++i)
+                                ph[i] = Words<T2>::make(r + 2 * i);
+                        } else if constexpr (bth) {
                             if constexpr (TM) {
                                 uint32_t r[32];
                                 tmem_ld32(lane_base + c0 * ((int)sizeof(T2) / 4), r);
@@ -617,7 +663,16 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                         sfor<0, EPC>([&](auto I) {
                             constexpr int mi = c0 + decltype(I)::value;
                             T2 a;
-                            if constexpr (odd) {
+                            if constexpr (odd && TWT) {
+                                // scale (conj(P) o + e): the table holds P unscaled
+                                Tw<T> w;
+                                w.lo = ph[decltype(I)::value];
+                                w.hi = w.lo;
+                                a = wide::cmul_tw<T, true>(v[mi], w);
+                                if constexpr (bth)
+                                    a = cadd(a, e[decltype(I)::value]);
+                                a = make_c<T>(a.x * scale, a.y * scale);
+                            } else if constexpr (odd) {
                                 a = PhaseR<T, R, true>::template apply<mi>(v[mi], pts);
                                 if constexpr (bth)
                                     a = fma_s<T>(e[decltype(I)::value], scale, a);
