@@ -671,13 +671,13 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                                 a = wide::cmul_tw<T, true>(v[mi], w);
                                 if constexpr (bth)
                                     a = cadd(a, e[decltype(I)::value]);
-                                a = make_c<T>(a.x * scale, a.y * scale);
+                                a = scale_c<T>(a, scale);
                             } else if constexpr (odd) {
                                 a = PhaseR<T, R, true>::template apply<mi>(v[mi], pts);
                                 if constexpr (bth)
                                     a = fma_s<T>(e[decltype(I)::value], scale, a);
                             } else {
-                                a = make_c<T>(v[mi].x * scale, v[mi].y * scale);
+                                a = scale_c<T>(v[mi], scale);
                             }
                             if (valid)
                                 yout[mi * TF] = a;

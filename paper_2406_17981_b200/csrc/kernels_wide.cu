@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
                 if (!uo) {
 #pragma unroll
                     for (int m = 0; m < R; ++m)
-                        dst[m * rs] = make_c<T>(scale * v[m].x, scale * v[m].y);
+                        dst[m * rs] = scale_c<T>(v[m], scale);
                     continue;
                 }
                 if constexpr (MODE == 1 && TM)
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
                 }
 #pragma unroll
                 for (int m = 0; m < R; ++m)
-                    dst[m * rs] = make_c<T>(scale * v[m].x, scale * v[m].y);
+                    dst[m * rs] = scale_c<T>(v[m], scale);
             }
         }
     }

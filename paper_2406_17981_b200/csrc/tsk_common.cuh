@@ -71,6 +71,16 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b)
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u(a)), "l"(f2_u(b)));
     return u_f2(d);
 }
+
+// v * s for a real s: one packed multiply for complex64
+template <typename T>
+__device__ __forceinline__ typename cx<T>::t scale_c(typename cx<T>::t v, T s)
+{
+    if constexpr (sizeof(T) == 4)
+        return mul2(v, make_float2(s, s));
+    else
+        return make_c<T>(v.x * s, v.y * s);
+}
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c)
 {
     unsigned long long d;
