@@ -370,10 +370,22 @@ def test_leaf_kernel_dyadic_vs_oracle(levels, prec, tol, storage):
     assert rel_l2(y, ys) <= tol
 
 
+def test_leaf_kernel_many_units_per_cta_vs_oracle():
+    # 33 x 25 = 825 mirror orbits: every CTA of the 512-point leaf pass (TMEM
+    # component exchange, twiddles and phases) loops over several units
+    levels = [64, 48, 512]
+    xs = _dyadic_x(levels, 23)
+    ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+    op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=T.C64)
+    assert op.info()["storage"] == T.STORAGE_COMPRESSED
+    assert rel_l2(op.apply(np.concatenate(xs)), ys) <= 1e-5
+
+
 @pytest.mark.parametrize("nparts", [2, 8])
-def test_leaf_kernel_partitions(nparts):
+@pytest.mark.parametrize("n", [256, 512])
+def test_leaf_kernel_partitions(nparts, n):
     # single-branch leaf passes (use_even / use_odd only) of the new kernel
-    levels = [4, 2, 256]
+    levels = [4, 2, n]
     xs = _dyadic_x(levels, 13)
     ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
     bg = T.BlockGenerator.dyadic(levels)
