@@ -236,19 +236,23 @@ constexpr bool leaf_mixt()
 #ifndef TSK_LEAF_TWT
 #define TSK_LEAF_TWT 1
 #endif
+// Stage-B twiddles (32 columns per radix-16 butterfly of a thread, R / 16 of
+// them) and the split phase (2R columns) in TMEM after the exchange blocks:
+// complex64, radix-16 stage B (N = 512 at R = 32, N = 256 at R = 16).
 template <typename T, int N, int R, int M, bool CMP, int NW>
 constexpr bool leaf_twt()
 {
     constexpr int EW = R * (int)sizeof(typename cx<T>::t) / 4;
-    return TSK_LEAF_TWT && leaf_mixt<T, R, M, CMP>() && sizeof(T) == 4 && R == 32 && N == 512 &&
-           2 * EW * ((NW + 3) / 4) + 128 <= 512;
+    return TSK_LEAF_TWT && leaf_mixt<T, R, M, CMP>() && sizeof(T) == 4 && N / R == 16 && R % 16 == 0 &&
+           2 * EW * ((NW + 3) / 4) + 64 * (R / 16) <= 512;
 }
-// TMEM columns per CTA: e' park (+ component exchange) for NW warps
-template <typename T, int R, int M, bool CMP, int NW>
+// TMEM columns per CTA: e' park (+ component exchange, + twiddles and phase)
+template <typename T, int N, int R, int M, bool CMP, int NW>
 constexpr int leaf_tcols()
 {
     constexpr int EW = R * (int)sizeof(typename cx<T>::t) / 4;
-    return tmem_cols_pow2(EW * ((NW + 3) / 4) * (leaf_mixt<T, R, M, CMP>() ? 2 : 1));
+    return tmem_cols_pow2(EW * ((NW + 3) / 4) * (leaf_mixt<T, R, M, CMP>() ? 2 : 1) +
+                          (leaf_twt<T, N, R, M, CMP, NW>() ? 64 * (R / 16) : 0));
 }
 
 // units (orbits) per CTA: warps per CTA a multiple of 4 (even split over the
@@ -307,13 +311,13 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     constexpr int EW = R * (int)sizeof(T2) / 4;
     constexpr bool TM = EW % 32 == 0;
     constexpr int NW = NT / 32 > 0 ? NT / 32 : 1;
-    constexpr int TCOLS = leaf_tcols<T, R, M, CMP, NW>();
+    constexpr int TCOLS = leaf_tcols<T, N, R, M, CMP, NW>();
     constexpr bool MIXT = leaf_mixt<T, R, M, CMP>();
     constexpr int MIXOFF = EW * ((NW + 3) / 4);  // first column of the exchange blocks
     // stage-B twiddles in TMEM (after the exchange blocks; 64 columns)
     constexpr bool TWT = leaf_twt<T, N, R, M, CMP, NW>();
     constexpr int TWOFF = 2 * MIXOFF;
-    constexpr int PHOFF = TWOFF + 64;  // phase table (TWT: 64 columns)
+    constexpr int PHOFF = TWOFF + 32 * (R / 16);  // phase table (TWT: 2R columns)
     uint32_t tbase = 0, lane_base = 0;
     if constexpr (TM) {
         tbase = tmem_alloc(&tmem_slot, TCOLS);
@@ -326,7 +330,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 const int tl = threadIdx.x % TF;
                 const uint32_t q = tbase + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16) + TWOFF;
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
+                for (int i = 0; i < R / 16; ++i) {
                     uint32_t r32[32];
 #pragma unroll
                     for (int r = 1; r < 16; ++r) {
@@ -347,7 +351,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                         r32[2 * i] = __float_as_uint(w.x);
                         r32[2 * i + 1] = __float_as_uint(w.y);
                     }
-                    tmem_st32(q + 64 + 32 * h, r32);
+                    tmem_st32(q + 32 * (R / 16) + 32 * h, r32);
                 }
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
@@ -732,7 +736,7 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         // TMEM: every resident CTA allocates its columns
         constexpr int EW = R * (int)sizeof(T2) / 4;
         constexpr int NW = NT / 32 > 0 ? NT / 32 : 1;
-        constexpr int TC = leaf_tcols<T, R, M, CMP, NW>();
+        constexpr int TC = leaf_tcols<T, N, R, M, CMP, NW>();
         if (EW % 32 == 0 && per_sm * TC > 512)
             per_sm = 512 / TC;
         if (getenv("TSK_DEBUG_OCC"))
