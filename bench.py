@@ -233,6 +233,7 @@ def run_b200(args):
     dom_ms = dom[1]["ms"] / dom[1]["n"]
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     traffic = None
+    limiter = None  # what bounds the dominant kernel when HBM does not (ncu pipes)
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
@@ -240,6 +241,7 @@ def run_b200(args):
         ent = tj.get(args.config, {}).get(dom[0])
         if ent:
             traffic = ent.get("dram_bytes_per_launch")
+            limiter = ent.get("limiter")
     es = info["elem_bytes"]
     compressed = info["storage"] == T.STORAGE_COMPRESSED
     balg, bvec, bk = b_alg(levels, m, info["n_unique"], es, compressed)
@@ -386,7 +388,7 @@ def run_b200(args):
                 "bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": bw_peak,
                 "unit": "GB/s", "frac": achieved / bw_peak, "traffic": traffic,
                 "alg_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
-                "peak_source": peak_src,
+                "peak_source": peak_src, "limiter": limiter,
             },
             "step_roofline": {
                 "B_alg_bytes": balg, "achieved_GBps": balg / (ms_per_step / 1e3) / 1e9 / world,
