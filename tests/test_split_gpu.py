@@ -522,3 +522,38 @@ def test_batch_device_apply_matches_single_applies():
     assert mb["fft_forward"] == 4 * m1["fft_forward"] and mb["diag_mults"] == 4 * m1["diag_mults"]
     with pytest.raises(T.TsError):
         op.apply_batch_device(x, x, 4)  # aliasing
+
+
+# ---- seeded shape fuzz: random level shapes mixing every kernel family
+# (wide strided tiles, 512/256-point leaf passes, generic mixed-radix and prime
+# axes) with all symmetry modes, both precisions, against the oracle
+def _fuzz_shapes(count, seed):
+    rng = np.random.default_rng(seed)
+    pool = [2, 3, 5, 7, 12, 16, 20, 31, 48, 64, 96, 128, 160, 256, 512]
+    fast = [64, 128, 256, 512]  # power-of-two lengths of the fast passes
+    shapes = []
+    while len(shapes) < count:
+        d = int(rng.integers(2, 5))
+        lv = [int(rng.choice(fast if rng.random() < 0.5 else pool)) for _ in range(d)]
+        if 4096 <= int(np.prod(lv)) <= 1_500_000:
+            shapes.append(lv)
+    return shapes
+
+
+@pytest.mark.parametrize("levels", _fuzz_shapes(12, 2024))
+def test_fuzz_shapes_vs_oracle(levels):
+    sym = [T.SYM_GENERAL, T.SYM_SYMMETRIC, T.SYM_SKEW][int(np.prod(levels)) % 3]
+    g = T.Generator.random(levels, 7, 1.0, sym)
+    lags, v, y_or = _oracle_split(levels, sym, 7)
+    assert rel_l2(T.Operator.split(g).apply(v), y_or) <= 1e-12
+    y64 = T.Operator.split_ex(T.BlockGenerator.from_scalar(g), precision=T.C64).apply(v)
+    assert rel_l2(y64, y_or) <= 1e-5
+
+
+@pytest.mark.parametrize("levels", [lv for lv in _fuzz_shapes(24, 77) if len(lv) == 3][:6])
+def test_fuzz_shapes_dyadic_vs_oracle(levels):
+    # the dyadic Green kernel is three-dimensional (component a <-> axis a)
+    xs = _dyadic_x(levels, 29)
+    ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+    op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=T.C64)
+    assert rel_l2(op.apply(np.concatenate(xs)), ys) <= 1e-5
