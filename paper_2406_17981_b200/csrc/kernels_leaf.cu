@@ -2,12 +2,17 @@
 // elements per thread: a length-N transform is two in-register stages (radix
 // R, then N/R) and ONE shared-memory exchange among the TF = N/R threads of a
 // (fiber, component) — a half or quarter warp, synchronised with __syncwarp.
-// The m x m spectra multiply couples the components through shared memory once
-// per branch; the even branch's output e' is parked in tensor memory (thread-
-// private lane) while the odd branch runs, and the odd branch re-reads x from
-// L2. A unit is one mirror orbit of 4 fibers (compressed spectra rows fetched
-// once, cp.async-staged) or, with full storage, 4 consecutive fibers (spectra
-// read straight from global memory, each element once), m components each.
+// The m x m spectra multiply couples the components once per branch: through
+// tensor memory (the component warps of a (fiber, t) share a TMEM lane; see
+// MIXT) with compressed storage, through shared memory otherwise. Tensor memory
+// also holds, per lane, the stage-B twiddles and the split phase (TWT), and
+// the even branch's output e' while the odd branch runs; the odd branch
+// re-reads x (an L1 hit). The pass is bound by the FP32 and L1/shared pipes,
+// not HBM, so TMEM serves as a second on-chip datapath (3x the shared-memory
+// read bandwidth, tools/micro/pipes.cu). A unit is one mirror orbit of 4
+// fibers (compressed spectra rows fetched once, cp.async-staged) or, with full
+// storage, 4 consecutive fibers (spectra read straight from global memory,
+// each element once), m components each.
 //
 // Reference semantics (relative to /root/reference/proj): leaf multiply
 // src/core/kernel.cpp:126-219, leaf FFT/IFFT and deepest merge
