@@ -744,9 +744,12 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         constexpr int TC = leaf_tcols<T, N, R, M, CMP, NW>();
         if (EW % 32 == 0 && per_sm * TC > 512)
             per_sm = 512 / TC;
-        if (getenv("TSK_DEBUG_OCC"))
-            fprintf(stderr, "k_leaf1<%d,%d,%d,%d>: %d CTAs/SM, %zu B smem, %d threads\n",
-                    (int)sizeof(T), N, R, M, per_sm, smem, NT);
+        if (getenv("TSK_DEBUG_OCC")) {
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, kern);
+            fprintf(stderr, "k_leaf1<%d,%d,%d,%d,%d>: %d CTAs/SM, %zu B smem (+%zu static), %d threads, %d regs\n",
+                    (int)sizeof(T), N, R, M, (int)CMP, per_sm, smem, fa.sharedSizeBytes, NT, fa.numRegs);
+        }
         cap = sm_count() * (per_sm > 0 ? per_sm : 1);
         cached_dev = dev;
     }
