@@ -270,7 +270,12 @@ constexpr int leaf1_g()
 }
 
 template <typename T, int N, int R, int M, bool CMP, int G = leaf1_g<N, R, M>()>
-__global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 * M * (N / R) < 384 ? 384 / (G * 4 * M * (N / R)) : 1) k_leaf1(tsk_axis p, tsk_spectra sp)
+// 16 elements per thread fit two 384-thread CTAs per SM (80 registers, 24
+// warps): the 256-point leaf 0.41 -> 0.365 ms at 256^3
+#ifndef TSK_LEAF256_2CTA
+#define TSK_LEAF256_2CTA 1
+#endif
+__global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 * M * (N / R) < 384 ? 384 / (G * 4 * M * (N / R)) : (TSK_LEAF256_2CTA && sizeof(T) == 4 && R == 16 && N == 256 ? 2 : 1)) k_leaf1(tsk_axis p, tsk_spectra sp)
 {
     using T2 = typename cx<T>::t;
     constexpr int TF = N / R;
@@ -736,14 +741,18 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         if (int e = (int)cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)smem))
             return e;
+        if (const char* cv = getenv("TSK_LEAF_CARVEOUT"))  // A/B: shared-memory carveout (%)
+            cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
-        // TMEM: every resident CTA allocates its columns
+        // TMEM: every resident CTA allocates its columns (the occupancy API
+        // undercounts tcgen05 kernels; tmem_occupancy counts the resources)
         constexpr int EW = R * (int)sizeof(T2) / 4;
         constexpr int NW = NT / 32 > 0 ? NT / 32 : 1;
         constexpr int TC = leaf_tcols<T, N, R, M, CMP, NW>();
-        if (EW % 32 == 0 && per_sm * TC > 512)
-            per_sm = 512 / TC;
+        if (EW % 32 == 0)
+            per_sm = tmem_occupancy(kern, NT, smem, TC);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
         if (getenv("TSK_DEBUG_OCC")) {
             cudaFuncAttributes fa{};
             cudaFuncGetAttributes(&fa, kern);

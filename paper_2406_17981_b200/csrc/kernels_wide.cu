@@ -152,9 +152,16 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
     constexpr int TCOLS = TCOLS_RAW <= 32 ? 32 : TCOLS_RAW <= 64 ? 64 : TCOLS_RAW <= 128 ? 128
                                                                         : TCOLS_RAW <= 256 ? 256 : 512;
     constexpr bool TM = PWORDS % 32 == 0;  // small R keeps B(e) in registers
-    const bool park = TM && MODE == 1 && ue && uo;
+// K1 keeps x in tensor memory for the even child instead of re-reading it
+// through L2 (with two CTAs per SM: K1 2.35/2.05 -> 2.09/1.94 ms at 512^3;
+// measured slower only while the occupancy API held tcgen05 kernels to one
+// CTA per SM)
+#ifndef WIDE_K1_XTMEM
+#define WIDE_K1_XTMEM 1
+#endif
+    const bool park = TM && (MODE == 1 || WIDE_K1_XTMEM) && ue && uo;
     uint32_t tbase = 0, lane_base = 0;
-    if constexpr (MODE == 1) {
+    if constexpr (MODE == 1 || WIDE_K1_XTMEM) {
         if (park) {
             tbase = tmem_alloc(&tmem_slot, TCOLS);
             const int warp = threadIdx.x / 32;
@@ -180,9 +187,22 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
             // src0 below the root), and the odd child needs the input again
             const T2* src = static_cast<const T2*>(p.src0) + base;
             if (uo) {
+#if WIDE_K1_XTMEM
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    v[m] = src[m * rs];
+                if constexpr (TM) {
+                    if (park)
+                        tmem_park<T, R>(lane_base, v);
+                }
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    v[m] = cmul_tw<T, false>(v[m], load_tw<T>(ph + t + m * TF));
+#else
 #pragma unroll
                 for (int m = 0; m < R; ++m)
                     v[m] = cmul_tw<T, false>(src[m * rs], load_tw<T>(ph + t + m * TF));
+#endif
                 fft_col<T, N, R, W, false>(v, buf, tw, t, w);
                 T2* dd = static_cast<T2*>(p.dst1) + base;
 #pragma unroll
@@ -190,10 +210,20 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
                     dd[m * rs] = v[m];
             }
             if (ue) {
-                // x again (L1/L2 hit; measured faster than a TMEM copy)
+                // x again: from TMEM (WIDE_K1_XTMEM), else an L1/L2 hit
+                bool have = false;
+#if WIDE_K1_XTMEM
+                if constexpr (TM) {
+                    if (park) {
+                        tmem_restore<T, R>(lane_base, v);
+                        have = true;
+                    }
+                }
+#endif
+                if (!have)
 #pragma unroll
-                for (int m = 0; m < R; ++m)
-                    v[m] = src[m * rs];
+                    for (int m = 0; m < R; ++m)
+                        v[m] = src[m * rs];
                 fft_col<T, N, R, W, false>(v, buf, tw, t, w);
                 T2* de = static_cast<T2*>(p.dst0) + base;
 #pragma unroll
@@ -248,7 +278,7 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
             }
         }
     }
-    if constexpr (MODE == 1) {
+    if constexpr (MODE == 1 || WIDE_K1_XTMEM) {
         if (park)
             tmem_free(tbase, TCOLS);
     }
@@ -289,7 +319,16 @@ static int launch(const tsk_axis& a, cudaStream_t st)
                                               (int)smem))
             return e;
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::NT, smem);
+        // K3 parks B(e) in TMEM: the occupancy API undercounts tcgen05
+        // kernels, so count the resources (TMEM columns included)
+        constexpr int PWORDS = G::R * (int)sizeof(T2) / 4;
+        constexpr int NW = G::NT / 32;
+        constexpr int TCR = PWORDS * ((NW + 3) / 4);
+        constexpr int TC = TCR <= 32 ? 32 : TCR <= 64 ? 64 : TCR <= 128 ? 128 : TCR <= 256 ? 256 : 512;
+        if ((MODE == 1 || WIDE_K1_XTMEM) && PWORDS % 32 == 0)
+            per_sm = tmem_occupancy(kern, G::NT, smem, TC);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::NT, smem);
         cap = sm_count() * (per_sm > 0 ? per_sm : 1);
         cached_dev = dev;
     }

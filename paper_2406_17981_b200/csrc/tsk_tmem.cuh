@@ -7,6 +7,8 @@
 
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "tsk_common.cuh"
 
 namespace tsk {
@@ -195,3 +197,34 @@ constexpr int tmem_cols_pow2(int n)
 }
 
 }  // namespace tsk
+
+#ifdef __CUDACC__
+namespace tsk {
+// CTAs per SM for a kernel that allocates tcols TMEM columns per CTA. The
+// occupancy API reports one CTA per SM for every tcgen05 kernel; measured on
+// B200 (tools/micro/tmem_coresidency.cu) the hardware co-schedules CTAs whose
+// allocations sum to <= 512 columns, so the limit is computed from registers,
+// shared memory, threads and TMEM columns directly.
+template <class K>
+static int tmem_occupancy(K kern, int nt, size_t dsmem, int tcols)
+{
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess)
+        return 1;
+    int dev = 0, regs_sm = 65536, smem_sm = 233472, thr_sm = 2048, resv = 1024;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
+    cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    const int warps = (nt + 31) / 32;
+    const int rpw = ((fa.numRegs * 32 + 255) / 256) * 256;  // registers per warp, allocation unit 256
+    int n = regs_sm / (rpw * warps);
+    n = std::min(n, smem_sm / (int)(dsmem + fa.sharedSizeBytes + resv));
+    n = std::min(n, thr_sm / (warps * 32));
+    if (tcols > 0)
+        n = std::min(n, 512 / tcols);
+    return n > 0 ? n : 1;
+}
+}  // namespace tsk
+#endif
