@@ -3,21 +3,23 @@
 //
 // Why wide tiles: a strided pass reads/writes, per tile, one contiguous row
 // segment per position along the axis. Measured on B200 (tools/micro/
-// strided_copy2.cu, pure 1R/2W copies of 512-row tiles): 64-byte segments
-// reach 2.3 TB/s, 128-byte 4.3 TB/s, 256-byte 5.8 TB/s (of 6.55 measured) —
-// independent of stride, TLB reach or tile order. So every warp memory
-// instruction here covers one 256-byte row segment (W = 32 complex64 or 16
-// complex128 columns), and a tile is N x 256 bytes (128 KB at N = 512).
+// strided_copy2.cu / strided_copy3.cu, pure 1R/2W copies of 512-row tiles):
+// 64-byte segments reach 2.3 TB/s, 128-byte 4.4-5.2 TB/s at two CTAs per SM,
+// 256-byte 5.7-5.8 TB/s at one. Every warp memory instruction covers one
+// row segment of W columns; the default is 128 bytes (W = 16 complex64) with
+// two CTAs per SM, so one CTA's memory phase overlaps the other's arithmetic.
 //
-// To fit that tile, each thread holds R = 16..32 elements of one column in
-// registers ("row pattern" k = t + m*TF, TF = N/R threads per column): N = 512
-// is 32 x 16, one shared-memory exchange per transform.
-//  K1: odd = F(P x) is transformed and stored (to the child buffer), then x
-//      is re-read (an L2 hit, the tile was just loaded) for even = F(x), which
-//      may overwrite x in place.
+// Each thread holds R = 16..32 elements of one column in registers ("row
+// pattern" k = t + m*TF, TF = N/R threads per column): N = 512 is 32 x 16, one
+// shared-memory exchange per transform.
+//  K1: odd = F(P x) is transformed and stored (to the child buffer), then
+//      even = F(x) from x parked in tensor memory (thread-private lane) when
+//      the load arrived — the even child may overwrite x in place.
 //  K3: out = scale * (B(e) + conj(P) B(o)); B(e) is parked in tensor memory
-//      (tcgen05.st/ld on the thread's own TMEM lane, 32x32b shape) while B(o)
-//      is computed, so registers hold one transform at a time.
+//      while B(o) is computed, so registers hold one transform at a time.
+// Both allocate TMEM, so the launcher counts CTAs per SM from registers,
+// shared memory and columns (the occupancy API reports one for tcgen05
+// kernels).
 // Reference semantics as in kernels_generic.cu (fft.cpp:65-87,
 // tensor.cpp:227-254, engine_split.cpp:13-37).
 #include <cuda_runtime.h>
@@ -340,8 +342,9 @@ static int launch(const tsk_axis& a, cudaStream_t st)
     return (int)cudaGetLastError();
 }
 
-// Row segment per tile: K1 (one input, two outputs) runs two 128-byte-wide
-// CTAs per SM, K3 (two inputs) one 256-byte-wide CTA; TSK_WIDE_SEG=128|256
+// Row segment per tile: 128 bytes, two CTAs per SM for K1 and K3 (with the
+// TMEM-aware occupancy: K3 at 512^3 1.89 -> 1.69 ms on axis 1, 1.90 -> 1.88 ms
+// on axis 0 against one 256-byte-wide CTA per SM); TSK_WIDE_SEG=128|256
 // overrides both (A/B).
 static int seg_bytes(int mode)
 {
@@ -352,7 +355,8 @@ static int seg_bytes(int mode)
     }
     if (v == 128 || v == 256)
         return v;
-    return mode == 0 ? 128 : 256;
+    (void)mode;
+    return 128;
 }
 
 template <typename T, int MODE, int SEG>
