@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
 
             if (beta == 0 && both) {
                 if constexpr (TM)
-                    tmem_park<T, R>(lane_base, v);
+                    tmem_park<T, R, false>(lane_base, v);  // waited before the restore
                 else
 #pragma unroll
                     for (int m = 0; m < R; ++m)
@@ -642,6 +642,8 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 T2* yout = dst + c * p.cstride + g * N + t;
                 auto emit = [&](auto ODD, auto BOTH) {
                     constexpr bool odd = decltype(ODD)::value, bth = decltype(BOTH)::value;
+                    if constexpr (bth && TM)
+                        tmem_wait_st();  // e' park (usually long complete)
                     sfor<0, R / EPC>([&](auto C) {
                         constexpr int c0 = decltype(C)::value * EPC;
                         T2 e[EPC], ph[TWT ? EPC : 1];

@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
                     v[m] = src[m * rs];
                 if constexpr (TM) {
                     if (park)
-                        tmem_park<T, R>(lane_base, v);
+                        tmem_park<T, R, false>(lane_base, v);  // waited before the restore
                 }
 #pragma unroll
                 for (int m = 0; m < R; ++m)
@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
 #if WIDE_K1_XTMEM
                 if constexpr (TM) {
                     if (park) {
+                        tmem_wait_st();
                         tmem_restore<T, R>(lane_base, v);
                         have = true;
                     }
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
                     continue;
                 }
                 if constexpr (MODE == 1 && TM)
-                    tmem_park<T, R>(lane_base, v);
+                    tmem_park<T, R, false>(lane_base, v);  // waited before the restore
                 else
 #pragma unroll
                     for (int m = 0; m < R; ++m)
@@ -264,8 +265,10 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
                     v[m] = cmul_tw<T, true>(v[m], load_tw<T>(ph + t + m * TF));
                 if (ue) {
                     T2 e[R];
-                    if constexpr (MODE == 1 && TM)
+                    if constexpr (MODE == 1 && TM) {
+                        tmem_wait_st();
                         tmem_restore<T, R>(lane_base, e);
+                    }
                     else
 #pragma unroll
                         for (int m = 0; m < R; ++m)

@@ -103,7 +103,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&r)[32])
 }
 
 // Park / restore R complex values (2 or 4 words each) in this thread's lane.
-template <typename T, int R>
+// WAIT = false leaves the stores in flight: the caller issues tmem_wait_st()
+// (or any later tcgen05.wait::st) before the values are read back.
+template <typename T, int R, bool WAIT = true>
 __device__ __forceinline__ void tmem_park(uint32_t lane_base, const typename cx<T>::t (&v)[R])
 {
     constexpr int WORDS = R * (int)sizeof(typename cx<T>::t) / 4;
@@ -117,7 +119,8 @@ __device__ __forceinline__ void tmem_park(uint32_t lane_base, const typename cx<
                                                  (c * 32 + i) % Words<typename cx<T>::t>::W);
         tmem_st32(lane_base + c * 32, r);
     }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    if constexpr (WAIT)
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
 template <typename T, int R>
