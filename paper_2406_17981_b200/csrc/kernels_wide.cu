@@ -346,10 +346,11 @@ static int launch(const tsk_axis& a, cudaStream_t st)
 }
 
 // Row segment per tile: 128 bytes, two CTAs per SM for K1 and K3 (with the
-// TMEM-aware occupancy: K3 at 512^3 1.89 -> 1.69 ms on axis 1, 1.90 -> 1.88 ms
-// on axis 0 against one 256-byte-wide CTA per SM); TSK_WIDE_SEG=128|256
-// overrides both (A/B).
-static int seg_bytes(int mode)
+// TMEM-aware occupancy: K3 at 512^3 1.89 -> 1.69 ms on axis 1 against one
+// 256-byte-wide CTA per SM); for axes whose row stride is >= 1 MB (axis 0 at
+// 512^3: 2 MB) one 256-byte CTA per SM is a little faster (K1 2.10 -> 2.05 ms,
+// K3 1.92 -> 1.88 ms). TSK_WIDE_SEG=128|256 overrides both (A/B).
+static int seg_bytes(int mode, int64_t stride_bytes)
 {
     static int v = -1;
     if (v < 0) {
@@ -359,7 +360,7 @@ static int seg_bytes(int mode)
     if (v == 128 || v == 256)
         return v;
     (void)mode;
-    return 128;
+    return stride_bytes >= (int64_t(1) << 20) ? 256 : 128;
 }
 
 template <typename T, int MODE, int SEG>
@@ -377,7 +378,9 @@ static int dispatch_seg(const tsk_axis& a, cudaStream_t st)
 template <typename T, int MODE>
 static int dispatch(const tsk_axis& a, cudaStream_t st)
 {
-    return seg_bytes(MODE) == 128 ? dispatch_seg<T, MODE, 128>(a, st) : dispatch_seg<T, MODE, 256>(a, st);
+    const int64_t stride_bytes = a.inner * (int64_t)sizeof(typename cx<T>::t);
+    return seg_bytes(MODE, stride_bytes) == 128 ? dispatch_seg<T, MODE, 128>(a, st)
+                                                : dispatch_seg<T, MODE, 256>(a, st);
 }
 
 }  // namespace wide
