@@ -315,12 +315,13 @@ def test_fast_and_generic_agree(levels, monkeypatch):
 
 
 @pytest.mark.parametrize("levels", [[512, 8, 32], [256, 32, 16], [128, 64, 32], [64, 64, 64],
-                                    [512, 3, 96], [3, 512, 96], [5, 128, 160]])
+                                    [512, 3, 96], [3, 512, 96], [5, 128, 160], [64, 512, 256]])
 def test_wide_strided_passes_vs_oracle(levels):
     # axes with n in {64..512} and 256-byte-multiple strides run the wide
     # tiles (kernels_wide.cu), including in-place K1 below the root and the
     # TMEM-parked K3; non-power-of-two column-block and outer counts exercise
-    # the multiply-high tile decomposition
+    # the multiply-high tile decomposition; [64, 512, 256] has a 1 MB row
+    # stride on axis 0 (256-byte row segments)
     for sym in (T.SYM_GENERAL, T.SYM_SYMMETRIC):
         g = T.Generator.random(levels, 21, 1.0, sym)
         lags, v, y_or = _oracle_split(levels, sym, 21)
