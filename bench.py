@@ -2,14 +2,19 @@
 """Benchmark: split-FFT block-Toeplitz MVM/s on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config c3|c3full|c2|c4|c1] [--no-e2e] [--no-cpu-baseline] [--embed-baseline]
+                    [--config c3|c3full|c2|c4|c1] [--no-e2e] [--no-cpu-baseline]
+                    [--no-embed-baseline]
 
 Default workload (N=1): BASELINE.json configs[3] — d=3, 512^3 grid, 3x3 dyadic
 Green kernel (configs[1] definition), complex64, mirror-compressed spectra,
-x i.i.d. CN(0,1) from the reference's RNG (seed 4). A "step" is one MVM
-y = T x through the library's device API (ts_operator_apply_device); at N>1
-each rank owns 1/N of the 2^d branches (ts_split_options.part/nparts) and the
-projected partials are summed with an NCCL reduce inside the step.
+x i.i.d. CN(0,1) from the reference's RNG (seed 4); operators and inputs come
+from paper_2406_17981_b200/workloads.py, the same ones the full-size parity
+tests check against the reference (tests/test_fullsize_gpu.py). A "step" is
+one MVM y = T x through the library's device API (ts_operator_apply_device).
+At N>1 each rank owns 1/N of the 2^d branches (ts_split_options.part/nparts)
+and ts_operator_apply_device_comm sums the projected partials with an NCCL
+reduce inside the library, in the step. `--gpus N` outside torchrun launches
+the N ranks itself.
 
 Under torchrun (N>1) every rank runs; rank 0 prints ONE JSON line. The
 reference arm (--impl reference) times the reference's own CPU code
@@ -31,14 +36,6 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIGS = {
-    # name: (levels, kind, precision, storage, x seed, BASELINE configs index)
-    "c3": ([512, 512, 512], "dyadic", "c64", "auto", 4, 3),
-    "c3full": ([512, 512, 512], "dyadic", "c64", "full", 4, 3),  # full 6-unique spectra
-    "c2": ([256, 256, 256], "dyadic", "c64", "auto", 3, 2),
-    "c1": ([64, 64, 64], "dyadic", "c64", "full", 2, 1),
-    "c4": ([64, 64, 64, 64], "scalar", "c64", "full", 6, 4),
-}
 METRIC = "Toeplitz MVM/s at 512³ 3×3 c64, 1/2/4/8 B200; % of HBM roofline"
 
 
@@ -121,35 +118,39 @@ def b_alg(levels, m, m_unique, es, compressed):
     return vec + k, vec, k
 
 
-def make_operator(T, cfg, part, nparts, device):
-    levels, kind, prec, storage, _, _ = cfg
-    st = {"auto": T.STORAGE_AUTO, "full": T.STORAGE_FULL, "compressed": T.STORAGE_COMPRESSED}[storage]
-    pr = T.C64 if prec == "c64" else T.C128
-    if kind == "dyadic":
-        bg = T.BlockGenerator.dyadic(levels)
-    else:
-        bg = None
-    if bg is None:
-        # configs[4]: non-symmetric CN(0,1) lags scaled by 1/(1+|m|_2), seed 5
-        import numpy as np
-        g = T.Generator.random(levels, 5, 0.5, T.SYM_GENERAL)
-        lags = g.lags()
-        grids = np.meshgrid(*[np.arange(-(n - 1), n) for n in levels], indexing="ij")
-        r = np.sqrt(sum(gr.astype(np.float64) ** 2 for gr in grids)).reshape(-1)
-        lags = lags / (1.0 + r)
-        bg = T.BlockGenerator.create(levels, 1, [0], [lags], [[0] * len(levels)])
-        del g
-    return T.Operator.split_ex(bg, precision=pr, storage=st, device=device, part=part,
-                               nparts=nparts)
+def free_port():
+    import socket
+
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    p = so.getsockname()[1]
+    so.close()
+    return p
 
 
-def gen_input(T, cfg):
-    """x i.i.d. CN(0,1) (variance 0.5 per part) from the reference RNG, SoA."""
-    import numpy as np
-    levels, kind, _, _, seed, _ = cfg
-    comp = 3 if kind == "dyadic" else 1
-    lv = ([comp] + list(levels)) if comp > 1 else list(levels)
-    return T.random_vector(lv, seed, 0.5).astype(np.complex128, copy=False)
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: launch N ranks (one per GPU) the way the
+    driver does, and pass their output through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.run(cmd).returncode)
+
+
+def family_profile(op, x, y, stream, steps):
+    """Per-launch device times (CUDA events on the launching stream) over the
+    same K MVMs, grouped by kernel family."""
+    recs = []
+    for _ in range(steps):
+        recs += op.profile_device(x, y, stream)
+    fam = {}
+    for r in recs:
+        key = {1: "fwd_split", 2: "leaf_pair", 3: "inv_merge"}.get(r["kind"], "other")
+        f = fam.setdefault(key, {"ms": 0.0, "bytes": 0, "n": 0})
+        f["ms"] += r["ms"]
+        f["bytes"] += r["alg_bytes"]
+        f["n"] += 1
+    return fam
 
 
 def run_b200(args):
@@ -158,47 +159,60 @@ def run_b200(args):
     import torch.distributed as dist
 
     import paper_2406_17981_b200 as T
+    from paper_2406_17981_b200 import partition
+    from paper_2406_17981_b200 import workloads as W
 
     world, rank, local = dist_env()
-    if world != args.gpus:
-        if not (world == 1 and args.gpus == 1):
-            print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = CONFIGS[args.config]
-    levels, kind, prec, storage, seed, cidx = cfg
+    name = args.config
+    levels, kind, prec, storage, _, _, cidx = W.CONFIGS[name]
     d = len(levels)
-    if world > 2 ** d:
-        raise SystemExit(f"at most 2^d = {2 ** d} GPUs (one branch each)")
+    s = math.prod(levels)
+    partition.check_world(world, d)
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- setup (not timed): operator with spectra precomputed on the device
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info(dev)[0]
+    mem0 = T.memory_stats(local)
+    T.reset_memory_peak(local)
     t0 = time.time()
-    op = make_operator(T, cfg, rank, world, local)
+    if world > 1:
+        pop = partition.PartitionedOperator(
+            T, lambda r, w, dv: W.make_operator(T, name, part=r, nparts=w, device=dv),
+            rank, world, local, d)
+        op = pop.op
+    else:
+        pop = None
+        op = W.make_operator(T, name, device=local)
     setup_s = time.time() - t0
+    setup_peak = T.memory_stats(local)["peak_bytes"] - mem0["live_bytes"]
     info = op.info()
     m = info["m"]
-    s = math.prod(levels)
     cdt = torch.complex64 if info["precision"] == T.C64 else torch.complex128
-    xh = gen_input(T, cfg)
-    x = torch.from_numpy(xh).to(dev).to(cdt)
+    xh = W.input_vector(T, name)  # reference RNG, complex128 host
+    x = torch.from_numpy(xh).to(cdt).to(dev)  # rounded on the host: no complex128 device copy
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream(dev)
 
-    from paper_2406_17981_b200 import partition
-
-    partition.check_world(world, d)
-
     def step():
-        op.apply_device(x, y, stream)
-        if world > 1:
-            partition.reduce_partials(y, dst=0)  # NCCL over NVLink
+        if pop is not None:
+            pop.apply(x, y, stream)  # subtree + NCCL reduce of the partials (in the library)
+        else:
+            op.apply_device(x, y, stream)
 
+    # ---- timed region: K MVMs on device-resident x, y
+    T.reset_memory_peak(local)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -208,41 +222,34 @@ def run_b200(args):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    barrier()
+    ms_t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     ms_per_step = ms / args.steps
-    value = args.steps / (ms / 1e3)  # MVM/s (one MVM per step for the whole job)
+    value = args.steps / (ms / 1e3)  # MVM/s of the whole job
 
-    # per-launch profile for the roofline: the same K MVMs again, with a CUDA
-    # event pair around every launch on the launching stream (kept out of the
-    # timed loop above so that `value` carries no event overhead)
-    recs = []
-    for _ in range(args.steps):
-        recs += op.profile_device(x, y, stream)
-    fam = {}
-    for r in recs:
-        key = {1: "fwd_split", 2: "leaf_pair", 3: "inv_merge"}.get(r["kind"], "other")
-        f = fam.setdefault(key, {"ms": 0.0, "bytes": 0, "n": 0})
-        f["ms"] += r["ms"]
-        f["bytes"] += r["alg_bytes"]
-        f["n"] += 1
+    # ---- device memory of the MVM, as the library meters it (spectra,
+    # tables, the schedule's child buffers) plus the caller's x and y
+    mem = T.memory_stats(local)
+    info = op.info()
+    peak_mvm = int(mem["peak_bytes"] + x.numel() * x.element_size() * 2)
+    used_delta = int(free0 - torch.cuda.mem_get_info(dev)[0])
+
+    # ---- per-launch profile for the roofline: the same K MVMs again with a
+    # CUDA event pair around every launch (kept out of the timed loop)
+    fam = family_profile(op, x, y, stream, args.steps)
     bw_peak, peak_src = peaks()
     dom = max(fam.items(), key=lambda kv: kv[1]["ms"])
     dom_bytes = dom[1]["bytes"] / dom[1]["n"]
     dom_ms = dom[1]["ms"] / dom[1]["n"]
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-    traffic = None
-    limiter = None  # what bounds the dominant kernel when HBM does not (ncu pipes)
+    traffic = limiter = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            tj = json.load(f)
-        ent = tj.get(args.config, {}).get(dom[0])
+            ent = json.load(f).get(name, {}).get(dom[0])
         if ent:
             traffic = ent.get("dram_bytes_per_launch")
             limiter = ent.get("limiter")
@@ -250,117 +257,36 @@ def run_b200(args):
     compressed = info["storage"] == T.STORAGE_COMPRESSED
     balg, bvec, bk = b_alg(levels, m, info["n_unique"], es, compressed)
 
-    # device memory of the MVM itself (operator + x, y + stream-ordered workspace),
-    # before the e2e section adds its second x/y pair
-    peak_mvm = torch.cuda.max_memory_allocated(dev)
-
-    # end-to-end through the public API: pinned host x -> device -> MVM
-    # (+ reduce) -> pinned host y, every step
+    # ---- end to end through the public API
     e2e = None
     if not args.no_e2e:
-        xp = torch.from_numpy(xh).to(cdt).pin_memory()
-        yp = torch.empty_like(xp).pin_memory()
-        ke = max(1, min(args.steps, 3))
+        if world == 1:
+            e2e = e2e_abi(op, xh, args)
+            e2e["device_api_pipelined"] = e2e_pipelined(op, x, y, xh, cdt, stream, args)
+        else:
+            e2e = e2e_comm(pop, x, y, xh, cdt, stream, args, rank, world, dev)
 
-        def e2e_step():
-            x.copy_(xp, non_blocking=True)
-            step()
-            if rank == 0:
-                yp.copy_(y, non_blocking=True)
-
-        e2e_step()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(ke):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        serial = ke / (float(ems.item()) / 1e3)
-        # pipelined across steps (how a serving loop would run it): H2D of step
-        # i+1 and D2H of step i-1 on their own copy streams (separate copy
-        # engines) while step i computes; two x and two y device buffers.
-        # Every step still moves its whole x in and its whole y out.
-        xs_ = [x, torch.empty_like(x)]
-        ys_ = [y, torch.empty_like(y)]
-        sh = torch.cuda.Stream(dev)
-        sd = torch.cuda.Stream(dev)
-        kp = max(3, args.steps)  # the same K steps as the device-resident number
-        in_ev = [torch.cuda.Event() for _ in range(2)]
-        used_ev = [torch.cuda.Event() for _ in range(2)]
-        out_ev = [torch.cuda.Event() for _ in range(2)]
-        done_ev = [torch.cuda.Event() for _ in range(2)]
-        for e in used_ev + done_ev:
-            e.record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        p0 = torch.cuda.Event(enable_timing=True)
-        p1 = torch.cuda.Event(enable_timing=True)
-        p0.record(sh)
-        for i in range(kp):
-            b = i % 2
-            sh.wait_event(used_ev[b])
-            with torch.cuda.stream(sh):
-                xs_[b].copy_(xp, non_blocking=True)
-            in_ev[b].record(sh)
-            stream.wait_event(in_ev[b])
-            stream.wait_event(done_ev[b])
-            op.apply_device(xs_[b], ys_[b], stream)
-            if world > 1:
-                partition.reduce_partials(ys_[b], dst=0)
-            used_ev[b].record(stream)
-            out_ev[b].record(stream)
-            sd.wait_event(out_ev[b])
-            if rank == 0:
-                with torch.cuda.stream(sd):
-                    yp.copy_(ys_[b], non_blocking=True)
-            done_ev[b].record(sd)
-        p1.record(sd)
-        torch.cuda.synchronize()
-        pms = torch.tensor([p0.elapsed_time(p1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(pms, op=dist.ReduceOp.MAX)
-        e2e = {"value": kp / (float(pms.item()) / 1e3), "unit": "MVM/s",
-               "h2d_bytes_per_step": int(xp.numel() * xp.element_size()),
-               "d2h_bytes_per_step": int(yp.numel() * yp.element_size()),
-               "steps": kp, "serial_value": serial,
-               "api": "pinned host x -> ts_operator_apply_device (+NCCL reduce) -> pinned host y; "
-                      "copies of neighbouring steps overlap on two copy streams (serial_value: "
-                      "one stream, no overlap)"}
-        del xs_[1], ys_[1]
-        # the reference-facing C-ABI call (ts_operator_apply, host complex128
-        # interleaved doubles, H2D/D2H inside the call) at N=1
-        if world == 1 and not args.no_abi_e2e:
-            xa = xh
-            t1 = time.perf_counter()
-            ya = op.apply(xa)
-            e2e["abi_ts_operator_apply_s"] = time.perf_counter() - t1
-            e2e["abi_h2d_bytes"] = int(xa.nbytes)
-            del ya
-        del xp, yp
-
+    # ---- the full-embedding cuFFT baseline (same run, same x), N=1
     emb = None
-    if args.embed_baseline and kind == "dyadic" and world == 1:
+    if world == 1 and kind == "dyadic" and not args.no_embed_baseline:
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         import embed_baseline
 
         op.apply_device(x, y, stream)
         torch.cuda.synchronize()
-        emb = embed_baseline.run(levels, x, y)
+        op.close()  # free the split operator's spectra and workspace first
+        del op
+        torch.cuda.empty_cache()
+        try:
+            emb = embed_baseline.run(levels, x, y, steps=max(2, min(args.steps, 5)), warmup=1)
+            emb["peak_device_bytes_vs_split"] = emb["peak_device_bytes"] / peak_mvm
+        except Exception as e:  # e.g. out of memory on a smaller GPU
+            emb = {"unavailable": f"{type(e).__name__}: {e}"[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = reference_sample(args, cfg)
+        cpu = reference_sample(args, name)
 
-    peak_mem = peak_mvm
-    peak_all = torch.cuda.max_memory_allocated(dev)
     if rank == 0:
         clocks = clk.summary()
         line = {
@@ -375,17 +301,20 @@ def run_b200(args):
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": "c64" if info["precision"] == T.C64 else "c128",
-            "data": "synthetic (reference SplitMix64/Box-Muller x, analytic dyadic kernel)",
+            "data": "synthetic (reference SplitMix64/Box-Muller x, analytic dyadic kernel)"
+                    if kind == "dyadic" else "synthetic (reference SplitMix64/Box-Muller lags and x)",
             "config": {
                 "workload": f"BASELINE.json configs[{cidx}]: d={d} {'x'.join(map(str, levels))} "
                             f"{'3x3 dyadic' if kind == 'dyadic' else 'scalar'} {prec}, "
                             f"{'mirror-compressed' if compressed else 'full'} spectra",
                 "levels": levels, "components": m, "unique_components": info["n_unique"],
                 "storage": "compressed" if compressed else "full",
-                "parallelism": f"branch partition over {world} GPU(s) + NCCL reduce" if world > 1
+                "parallelism": f"branch partition over {world} GPUs, NCCL broadcast/reduce inside "
+                               "libtoesplit (ts_operator_apply_device_comm)" if world > 1
                 else "1 GPU, whole tree",
                 "l2": "inputs (%.2f GB per vector) larger than the 126 MB L2; no flush needed"
-                      % (m * s * es / 1e9),
+                      % (m * s * es / 1e9) if m * s * es > 126e6 else
+                      "working set partly L2-resident (vectors %.1f MB); no flush" % (m * s * es / 1e6),
                 "B_alg_bytes_per_mvm": balg,
             },
             "roofline": {
@@ -403,35 +332,161 @@ def run_b200(args):
             },
             "kernel_families": {k: {"launches": v["n"] // args.steps, "ms": v["ms"] / args.steps,
                                     "GBps": v["bytes"] / (v["ms"] / 1e3) / 1e9}
-                                for k, v in fam.items()},  # per MVM
+                                for k, v in fam.items()},  # per MVM (rank 0's share at N > 1)
             "gpu_launches": int(info["launches"]) * args.steps,
             "e2e": e2e,
             "embed_baseline": emb,
             "cpu_baseline": cpu,
             "clocks": clocks,
-            "peak_device_bytes": int(peak_mem),
-            "peak_device_bytes_incl_e2e_buffers": int(peak_all),
-            "spectra_bytes": int(info["spectra_bytes"]),
+            "peak_device_bytes": peak_mvm,
+            "memory": {
+                "peak_device_bytes": peak_mvm,
+                "how": "libtoesplit device meter (ts_device_memory_stats peak over warm-up + timed "
+                       "MVMs: spectra + tables + cached child buffers) + caller x and y",
+                "library_peak_bytes": int(mem["peak_bytes"]),
+                "spectra_bytes": int(info["spectra_bytes"]),
+                "table_bytes": int(info["table_bytes"]),
+                "workspace_bytes": int(info["cached_bytes"]),
+                "x_y_bytes": int(2 * x.numel() * x.element_size()),
+                "cuda_mem_get_info_delta_bytes": used_delta,
+                "setup_peak_bytes": int(setup_peak),
+                "per_gpu": world > 1,
+            },
             "setup_s": setup_s,
         }
         print(json.dumps(line))
+    if pop is not None:
+        pop.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def e2e_abi(op, xh, args):
+    """The reference-facing call: ts_operator_apply on host complex128
+    interleaved buffers (ref proj/include/toesplit.h:131-132), H2D / D2H and
+    the precision conversion inside the call; the caller reuses its y."""
+    import numpy as np
+
+    ya = np.empty_like(xh)
+    t = time.perf_counter()
+    op.apply(xh, out=ya)  # first call: pinned staging pool, y pages touched
+    first = time.perf_counter() - t
+    ts = []
+    for _ in range(max(2, min(args.steps, 5))):
+        t = time.perf_counter()
+        _, mt = op.apply(xh, out=ya, metrics=True)
+        ts.append(time.perf_counter() - t)
+    med = statistics.median(ts)
+    return {"value": 1.0 / med, "unit": "MVM/s", "h2d_bytes_per_step": int(xh.nbytes),
+            "d2h_bytes_per_step": int(ya.nbytes), "steps": len(ts), "seconds_per_call": ts,
+            "first_call_s": first, "apply_ns_device": int(mt["apply_ns"]),
+            "api": "ts_operator_apply (the reference ABI call): pageable host complex128 x in, "
+                   "y out; staging, c128<->c64 rounding, H2D, MVM, D2H inside the call; "
+                   "host wall clock per call, median"}
+
+
+def e2e_pipelined(op, x, y, xh, cdt, stream, args):
+    """Pinned host x -> device -> ts_operator_apply_device -> pinned host y
+    every step, copies of neighbouring steps on two copy streams."""
+    import torch
+
+    dev = x.device
+    xp = torch.from_numpy(xh).to(cdt).pin_memory()
+    yp = torch.empty_like(xp).pin_memory()
+    xs_ = [x, torch.empty_like(x)]
+    ys_ = [y, torch.empty_like(y)]
+    sh, sd = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    kp = max(3, args.steps)
+    in_ev = [torch.cuda.Event() for _ in range(2)]
+    used_ev = [torch.cuda.Event() for _ in range(2)]
+    out_ev = [torch.cuda.Event() for _ in range(2)]
+    done_ev = [torch.cuda.Event() for _ in range(2)]
+    for e in used_ev + done_ev:
+        e.record(stream)
+    torch.cuda.synchronize()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(sh)
+    for i in range(kp):
+        b = i % 2
+        sh.wait_event(used_ev[b])
+        with torch.cuda.stream(sh):
+            xs_[b].copy_(xp, non_blocking=True)
+        in_ev[b].record(sh)
+        stream.wait_event(in_ev[b])
+        stream.wait_event(done_ev[b])
+        op.apply_device(xs_[b], ys_[b], stream)
+        used_ev[b].record(stream)
+        out_ev[b].record(stream)
+        sd.wait_event(out_ev[b])
+        with torch.cuda.stream(sd):
+            yp.copy_(ys_[b], non_blocking=True)
+        done_ev[b].record(sd)
+    p1.record(sd)
+    torch.cuda.synchronize()
+    val = kp / (p0.elapsed_time(p1) / 1e3)
+    del xs_[1], ys_[1]
+    return {"value": val, "unit": "MVM/s", "h2d_bytes_per_step": int(xp.numel() * xp.element_size()),
+            "d2h_bytes_per_step": int(yp.numel() * yp.element_size()), "steps": kp,
+            "api": "pinned host complex64 x -> ts_operator_apply_device -> pinned host y; copies of "
+                   "neighbouring steps overlap on two copy streams (CUDA events)"}
+
+
+def e2e_comm(pop, x, y, xh, cdt, stream, args, rank, world, dev):
+    """N > 1: pinned host x -> rank 0 -> NCCL broadcast + subtrees + reduce
+    (ts_operator_apply_device_comm) -> rank 0 -> pinned host y, every step."""
+    import torch
+    import torch.distributed as dist
+
+    xp = torch.from_numpy(xh).to(cdt).pin_memory() if rank == 0 else None
+    yp = torch.empty_like(xp).pin_memory() if rank == 0 else None
+
+    def one():
+        if rank == 0:
+            x.copy_(xp, non_blocking=True)
+        pop.apply(x, y, stream, bcast_x=True)
+        if rank == 0:
+            yp.copy_(y, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    dist.barrier()
+    k = max(2, min(args.steps, 5))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    nb = x.numel() * x.element_size()
+    return {"value": k / (float(t.item()) / 1e3), "unit": "MVM/s", "h2d_bytes_per_step": int(nb),
+            "d2h_bytes_per_step": int(nb), "steps": k,
+            "api": "pinned host x -> rank 0 -> ts_operator_apply_device_comm (NCCL broadcast, "
+                   "subtrees, reduce) -> rank 0 -> pinned host y; serial, CUDA events, max over ranks"}
+
+
+SAMPLE_N = {"c0": 16, "c1": 64, "c1_128": 64, "c2": 128, "c3": 128, "c3full": 128, "c4": 32}
+CALIBRATION = os.path.join(ROOT, "profiles", "r02_reference_fullsize.json")
 
 
 class RefSampler:
     """The UNMODIFIED reference (oracle/_ref) on host cores, on a bounded sample
     of the workload (same config, levels shrunk to sample_n per axis), built
     once; one() runs one sample MVM. Times are extrapolated to the full size
-    with the reference's own C_split cost model (ts_predict)."""
+    with the reference's own C_split cost model (ts_predict) and, where a
+    full-size run of the reference was measured on a box of this kind
+    (profiles/r02_reference_fullsize.json), corrected by the model's measured
+    error at that size."""
 
-    def __init__(self, cfg, sample_n):
-        import numpy as np
-
+    def __init__(self, name, sample_n):
         import oracle
+        from paper_2406_17981_b200 import workloads as W
 
-        levels, kind, _, _, seed, _ = cfg
-        self.levels, self.kind, self.n = levels, kind, sample_n
+        levels, kind, _, _, lag_seed, seed, _ = W.CONFIGS[name]
+        self.name, self.levels, self.kind, self.n = name, levels, kind, sample_n
         d = len(levels)
         slv = [sample_n] * d
         self.ncores = os.cpu_count() or 1
@@ -440,7 +495,7 @@ class RefSampler:
         s = math.prod(slv)
         self.ops = []
         if kind == "dyadic":
-            x = O.random_vector([3] + slv, seed, 0.5)
+            x = R.random_vector([3] + slv, seed, 0.5)
             self.xs = [x[i * s:(i + 1) * s] for i in range(3)]
             for i in range(3):
                 for j in range(i, 3):
@@ -449,7 +504,10 @@ class RefSampler:
                     self.ops.append((i, j, R.split(g)))
                     R.destroy_gen(g)
         else:
-            g = R.generator(slv, seed=5, symmetry=0, variance=0.5)
+            lags = O.random_lags(slv, lag_seed, 0.5, oracle.SYM_GENERAL)
+            if kind == "scaled":
+                lags = W.scale_lags_by_offset(lags, slv)
+            g = R.generator(slv, lags, oracle.SYM_GENERAL)
             self.xs = R.random_vector(slv, seed, 0.5)
             self.ops.append((0, 0, R.split(g)))
             R.destroy_gen(g)
@@ -457,6 +515,12 @@ class RefSampler:
         c_full = O.predict(d, float(levels[0]))["c_split"]
         c_samp = O.predict(d, float(sample_n))["c_split"]
         self.scale = c_full / c_samp
+        self.calib = None
+        if sample_n < levels[0] and os.path.exists(CALIBRATION):
+            with open(CALIBRATION) as f:
+                ent = json.load(f).get(name)
+            if ent and ent.get("sample_n") == sample_n and ent.get("host_cores") == self.ncores:
+                self.calib = ent
 
     def one(self, parallel=None, ops=None):
         import numpy as np
@@ -475,6 +539,11 @@ class RefSampler:
         else:
             R.apply(ops[0][2], self.xs, parallel=nc)
         return time.perf_counter() - t0
+
+    def full_seconds(self, t_sample):
+        """Estimated seconds per full-size MVM from a sample time."""
+        k = self.calib["model_correction"] if self.calib else 1.0
+        return t_sample * self.scale * k
 
     def extras(self):
         """SURVEY.md §8(d) companions at the sample size: the same MVM with the
@@ -519,24 +588,32 @@ class RefSampler:
         d = len(self.levels)
         what = ("3x3 dyadic (9 scalar reference applies, G_ii symmetric, G_ij general)"
                 if self.kind == "dyadic" else "scalar")
-        return {
-            "value": 1.0 / (t * self.scale), "unit": "MVM/s", "cores": self.ncores, "kind": "reference",
+        full = self.full_seconds(t)
+        out = {
+            "value": 1.0 / full, "unit": "MVM/s", "cores": self.ncores, "kind": "reference",
             "sample": f"{what} MVM at {self.n}^{d}, c128 (the reference's only precision), "
-                      f"TS_POLICY_PARALLEL task_budget={self.ncores}; median {t:.3f} s over {reps} rep(s), "
-                      f"extrapolated x{self.scale:.1f} to {self.levels[0]}^{d} by the reference's C_split model",
+                      f"TS_POLICY_PARALLEL task_budget={self.ncores}; median {t:.3f} s over {reps} rep(s)"
+                      + (f", extrapolated x{self.scale:.1f} to {self.levels[0]}^{d} by the reference's "
+                         "C_split model" if self.scale != 1.0 else " (full size)")
+                      + (f" and corrected x{self.calib['model_correction']:.3f} by the model's error "
+                         "against a measured full-size run" if self.calib else ""),
             "sample_seconds": t,
+            "full_size_seconds_estimate": full,
             "fft": "reference engine + substitute FFT (FFTW-API shim, FFTW3 absent)",
         }
+        if self.calib:
+            out["calibration"] = self.calib
+        return out
 
 
-def ref_sample_n():
-    return int(os.environ.get("TS_REF_SAMPLE_N", "128"))
+def ref_sample_n(name):
+    return int(os.environ.get("TS_REF_SAMPLE_N", SAMPLE_N.get(name, 128)))
 
 
-def reference_sample(args, cfg, budget_s=12.0):
+def reference_sample(args, name, budget_s=12.0):
     """cpu_baseline: repeat the sample MVM for about budget_s seconds of CPU work."""
     try:
-        smp = RefSampler(cfg, ref_sample_n())
+        smp = RefSampler(name, ref_sample_n(name))
     except Exception as e:  # reference build absent
         return {"unavailable": f"oracle/_ref not built: {e}"}
     try:
@@ -554,14 +631,16 @@ def reference_sample(args, cfg, budget_s=12.0):
 
 
 def run_reference(args):
+    from paper_2406_17981_b200 import workloads as W
+
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
-    levels, kind, prec, _, _, cidx = cfg
+    name = args.config
+    levels, kind, prec, _, _, _, cidx = W.CONFIGS[name]
     t0 = time.perf_counter()
     try:
-        smp = RefSampler(cfg, ref_sample_n())
+        smp = RefSampler(name, ref_sample_n(name))
     except Exception as e:
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
         return
@@ -569,15 +648,16 @@ def run_reference(args):
     for i in range(args.warmup + args.steps):
         t = smp.one()
         if i >= args.warmup:
-            per.append(t * smp.scale)
+            per.append(smp.full_seconds(t))
     smp.close()
-    base = smp.describe(statistics.median(per) / smp.scale, len(per))
+    base = smp.describe(statistics.median(per) / (smp.full_seconds(1.0)), len(per))
     t_step = statistics.mean(per)
     value = 1.0 / t_step
     base["value"] = value
     line = {
         "metric": METRIC, "impl": "reference", "value": value, "unit": "MVM/s",
-        "n_gpus": args.gpus, "host_cores": os.cpu_count(), "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "n_gpus": args.gpus, "host_cores": os.cpu_count(), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (reference SplitMix64/Box-Muller x, analytic dyadic kernel)",
         "config": {"workload": f"BASELINE.json configs[{cidx}] on host cores (sampled)",
@@ -590,20 +670,23 @@ def run_reference(args):
 
 
 def main():
+    from paper_2406_17981_b200 import workloads as W
+
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(W.CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-abi-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--embed-baseline", action="store_true",
-                    help="also time the full-embedding MVM with cuFFT (dyadic configs; ~120 GB)")
+    ap.add_argument("--no-embed-baseline", action="store_true",
+                    help="skip the full-embedding cuFFT MVM (dyadic configs; ~110 GB at 512^3)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("note: the timing rules ask for >= 3 warm-up steps", file=sys.stderr)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -114,6 +114,12 @@ typedef struct ts_operator_info {
     uint64_t spectra_bytes;    /* device bytes of stored spectra */
     uint64_t workspace_bytes;  /* device working set of one apply_device call */
     uint64_t launches;         /* kernels per apply_device call */
+    uint64_t table_bytes;      /* device bytes of twiddle / phase tables */
+    uint64_t cached_bytes;     /* device bytes held by the operator's apply contexts
+                                  (workspace kept across calls, host-path buffers) */
+    uint64_t graph_replays;    /* applies served by a captured CUDA graph */
+    int32_t ndevices;          /* 1, or P for a multi-GPU operator */
+    int32_t reserved2;
 } ts_operator_info;
 
 ts_status ts_operator_get_info(const ts_operator* op, ts_operator_info* out);
@@ -138,6 +144,59 @@ ts_status ts_operator_profile_device(const ts_operator* op, const void* x, void*
 
 /* Number of visible CUDA devices (0 when none); never fails. */
 int32_t ts_device_count(void);
+
+/* Device-memory meter (the reference's AllocationMeter, ref
+ * proj/src/core/tensor.cpp:49-66, for device bytes): every device buffer the
+ * library allocates on `device` — spectra, tables, apply workspaces, staging —
+ * counted live, by kind, with a high-water mark since the last reset.
+ * Caller-owned buffers (x, y of apply_device) are not included. */
+typedef struct ts_memory_stats {
+    uint64_t live_bytes;
+    uint64_t peak_bytes;
+    uint64_t spectra_bytes;
+    uint64_t table_bytes;
+    uint64_t workspace_bytes;
+    uint64_t staging_bytes;
+} ts_memory_stats;
+
+ts_status ts_device_memory_stats(int32_t device, ts_memory_stats* out);
+/* peak := live */
+ts_status ts_device_memory_reset_peak(int32_t device);
+
+/* ---- multi-GPU: the 2^d branches partitioned over P = 2^q GPUs -----------
+ * (the paper's outlook PAPER.md:97-99). GPU g owns the branch
+ * ids whose low q bits equal g, stores only their spectra, runs q single-child
+ * path levels, its subtree and q single-child inverse levels; the projected
+ * partial outputs are summed by one NCCL reduce over NVLink, component by
+ * component as the last inverse-merge pass finishes each (reduce of
+ * component c overlaps the pass of component c+1). NCCL is loaded at run time
+ * (libnccl.so.2); without it these calls fail with TS_ERR_RESOURCE. */
+
+/* One process driving P GPUs. devices[0..ndev) (ndev a power of two <= 2^d,
+ * distinct ordinals) receive parts 0..ndev-1; opt->part / opt->nparts /
+ * opt->device are ignored. ts_operator_apply and ts_operator_apply_device
+ * (x, y on devices[0], stream on devices[0]) then compute the whole product:
+ * x is broadcast from devices[0], partials are reduced onto devices[0]. */
+ts_status ts_operator_create_split_multi(const ts_block_generator* g, const ts_split_options* opt,
+                                         int32_t ndev, const int32_t* devices, ts_operator** out);
+
+/* One process per GPU (torchrun style): an NCCL communicator the library
+ * owns. Rank 0 calls ts_comm_unique_id, ships the 128 bytes to the other
+ * ranks out of band, and every rank calls ts_comm_create (collective). */
+typedef struct ts_comm ts_comm;
+ts_status ts_comm_unique_id(unsigned char out[128]);
+ts_status ts_comm_create(const unsigned char id[128], int32_t nranks, int32_t rank, int32_t device,
+                         ts_comm** out);
+void ts_comm_destroy(ts_comm* comm);
+
+/* Collective apply of a partition operator (part == rank, nparts == nranks,
+ * created on the communicator's device). bcast_x != 0: x is valid on root
+ * only and is broadcast into every rank's x buffer first; otherwise every
+ * rank holds x. On root y receives the whole product, elsewhere y holds the
+ * rank's partial (scratch). Asynchronous on stream like apply_device. */
+ts_status ts_operator_apply_device_comm(const ts_operator* op, ts_comm* comm, const void* x, void* y,
+                                        int32_t root, int32_t bcast_x, void* stream,
+                                        ts_metrics* metrics);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,10 @@ typedef struct tsk_axis {
     double scale; /* K3/K2 output scale (1/(2n) for a merge) */
     int32_t nrad;
     int32_t rad[TSK_MAX_RADICES];
+    /* K2 only: right-hand sides of a batched leaf pass (0 or 1 = one), the
+     * ncomp coupled components of RHS r start rstride elements after RHS r-1 */
+    int64_t nrhs;
+    int64_t rstride;
 } tsk_axis;
 
 /* Spectra description for the leaf pass (leaf axis = d-1, inner = 1). */

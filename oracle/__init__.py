@@ -79,6 +79,8 @@ class Oracle:
         L.orc_random_vector.argtypes = [C.c_int, _i64p, C.c_uint64, C.c_double, _dp]
         L.orc_dyadic_lags.argtypes = [C.c_int, _i64p, C.c_int, C.c_int, C.c_double, C.c_double,
                                       C.c_double, _dp]
+        L.orc_dyadic_lags_slab.argtypes = [C.c_int, _i64p, C.c_int, C.c_int, C.c_double,
+                                           C.c_double, C.c_double, C.c_int64, C.c_int64, _dp]
         L.orc_validate_symmetry.argtypes = [C.c_int, _i64p, _dp, _ip]
         L.orc_spectra_elems.argtypes = [C.c_int, _i64p, C.c_int]
         L.orc_spectra_elems.restype = C.c_int64
@@ -115,11 +117,27 @@ class Oracle:
                  "random_vector")
         return out
 
-    def dyadic_lags(self, levels, i, j, k=2 * np.pi / 10, self_term=1 + 0.1j):
+    def dyadic_lags(self, levels, i, j, k=2 * np.pi / 10, self_term=1 + 0.1j, threads=1):
         lv, lp = _lv(levels)
-        out = np.zeros(int(np.prod(2 * lv - 1)), np.complex128)
-        self._ok(self.L.orc_dyadic_lags(len(lv), lp, i, j, k, self_term.real, self_term.imag,
-                                        out.ctypes.data_as(_dp)), "dyadic_lags")
+        out = np.empty(int(np.prod(2 * lv - 1)), np.complex128)
+        rows = int(2 * lv[0] - 1)
+        if threads <= 1 or rows < 2:
+            self._ok(self.L.orc_dyadic_lags(len(lv), lp, i, j, k, self_term.real, self_term.imag,
+                                            out.ctypes.data_as(_dp)), "dyadic_lags")
+            return out
+        # axis-0 slabs on several threads (ctypes releases the GIL)
+        from concurrent.futures import ThreadPoolExecutor
+
+        cuts = np.linspace(0, rows, min(threads, rows) + 1).astype(np.int64)
+        op = out.ctypes.data_as(_dp)
+
+        def slab(t):
+            return self.L.orc_dyadic_lags_slab(len(lv), lp, i, j, k, self_term.real,
+                                               self_term.imag, int(cuts[t]), int(cuts[t + 1]), op)
+
+        with ThreadPoolExecutor(len(cuts) - 1) as ex:
+            for st in ex.map(slab, range(len(cuts) - 1)):
+                self._ok(st, "dyadic_lags_slab")
         return out
 
     def validate_symmetry(self, levels, lags, signs):

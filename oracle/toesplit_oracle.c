@@ -209,6 +209,15 @@ int orc_random_vector(int d, const int64_t* levels, uint64_t seed, double varian
 int orc_dyadic_lags(int d, const int64_t* levels, int i, int j, double k, double self_re,
                     double self_im, double* out)
 {
+    return orc_dyadic_lags_slab(d, levels, i, j, k, self_re, self_im, 0, 2 * levels[0] - 1, out);
+}
+
+/* The same values for the axis-0 lag rows [row0, row1) only (written at their
+ * place in the full tensor), so a caller can fill one tensor from several
+ * threads. */
+int orc_dyadic_lags_slab(int d, const int64_t* levels, int i, int j, double k, double self_re,
+                         double self_im, int64_t row0, int64_t row1, double* out)
+{
     int st = check_levels(d, levels);
     if (st)
         return st;
@@ -217,10 +226,14 @@ int orc_dyadic_lags(int d, const int64_t* levels, int i, int j, double k, double
     int64_t lag_shape[32];
     for (int a = 0; a < d; ++a)
         lag_shape[a] = 2 * levels[a] - 1;
-    const int64_t total = volume(d, lag_shape);
+    if (row0 < 0 || row1 > lag_shape[0] || row0 > row1)
+        return ORC_EINVAL;
+    const int64_t row = volume(d, lag_shape) / lag_shape[0];
+    const int64_t total = row1 * row;
     int64_t idx[32] = {0};
+    idx[0] = row0;
     const double delta = i == j ? 1.0 : 0.0;
-    for (int64_t off = 0; off < total; ++off) {
+    for (int64_t off = row0 * row; off < total; ++off) {
         double r2 = 0.0;
         for (int a = 0; a < d; ++a) {
             const double m = (double)(idx[a] - (levels[a] - 1));

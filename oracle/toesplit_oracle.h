@@ -42,6 +42,8 @@ int orc_random_vector(int d, const int64_t* levels, uint64_t seed, double varian
  * lags, k = wavenumber, self term (self_re + i self_im) * delta_ij. */
 int orc_dyadic_lags(int d, const int64_t* levels, int i, int j, double k, double self_re,
                     double self_im, double* out_lags);
+int orc_dyadic_lags_slab(int d, const int64_t* levels, int i, int j, double k, double self_re,
+                         double self_im, int64_t row0, int64_t row1, double* out);
 
 /* Exact per-axis symmetry check (proj/src/core/generator.cpp:38-62). */
 int orc_validate_symmetry(int d, const int64_t* levels, const double* lags, const int* axis_sign);

@@ -44,6 +44,8 @@ EXTENSION_SYMBOLS = [
     "ts_block_generator_components", "ts_block_generator_destroy", "ts_split_options_default",
     "ts_operator_create_split_ex", "ts_operator_apply_device", "ts_operator_apply_batch_device", "ts_operator_get_info",
     "ts_device_count", "ts_operator_profile_device", "ts_generator_get_lags",
+    "ts_device_memory_stats", "ts_device_memory_reset_peak", "ts_operator_create_split_multi",
+    "ts_comm_unique_id", "ts_comm_create", "ts_comm_destroy", "ts_operator_apply_device_comm",
 ]
 LAUNCHER_SYMBOLS = [
     "tsk_fwd_split", "tsk_inv_merge", "tsk_leaf_pair", "tsk_embed_generator", "tsk_embed_dyadic",
@@ -84,7 +86,18 @@ class TsOperatorInfo(C.Structure):
                 ("device", C.c_int32), ("part", C.c_int32), ("nparts", C.c_int32),
                 ("reserved", C.c_int32), ("elem_bytes", C.c_uint64),
                 ("spectra_bytes", C.c_uint64), ("workspace_bytes", C.c_uint64),
-                ("launches", C.c_uint64)]
+                ("launches", C.c_uint64), ("table_bytes", C.c_uint64),
+                ("cached_bytes", C.c_uint64), ("graph_replays", C.c_uint64),
+                ("ndevices", C.c_int32), ("reserved2", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class TsMemoryStats(C.Structure):
+    _fields_ = [("live_bytes", C.c_uint64), ("peak_bytes", C.c_uint64),
+                ("spectra_bytes", C.c_uint64), ("table_bytes", C.c_uint64),
+                ("workspace_bytes", C.c_uint64), ("staging_bytes", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -149,6 +162,15 @@ def _load():
     L.ts_device_count.restype = C.c_int32
     L.ts_operator_profile_device.argtypes = [_vp, _vp, _vp, _vp, C.POINTER(TsLaunchRecord),
                                              C.c_int32, C.POINTER(C.c_int32)]
+    L.ts_device_memory_stats.argtypes = [C.c_int32, C.POINTER(TsMemoryStats)]
+    L.ts_device_memory_reset_peak.argtypes = [C.c_int32]
+    L.ts_operator_create_split_multi.argtypes = [_vp, C.POINTER(TsSplitOptions), C.c_int32,
+                                                 C.POINTER(C.c_int32), C.POINTER(_vp)]
+    L.ts_comm_unique_id.argtypes = [C.c_char_p]
+    L.ts_comm_create.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_vp)]
+    L.ts_comm_destroy.argtypes = [_vp]
+    L.ts_operator_apply_device_comm.argtypes = [_vp, _vp, _vp, _vp, C.c_int32, C.c_int32, _vp,
+                                                C.POINTER(TsMetrics)]
     return L
 
 
@@ -174,6 +196,45 @@ def version() -> str:
 
 def device_count() -> int:
     return int(lib.ts_device_count())
+
+
+def memory_stats(device: int = 0) -> dict:
+    """The library's device-memory meter (ts_device_memory_stats)."""
+    m = TsMemoryStats()
+    _ok(lib.ts_device_memory_stats(device, C.byref(m)))
+    return m.as_dict()
+
+
+def reset_memory_peak(device: int = 0) -> None:
+    _ok(lib.ts_device_memory_reset_peak(device))
+
+
+class Comm:
+    """ts_comm: a library-owned NCCL communicator, one rank per process
+    (torchrun layout). Rank 0 calls unique_id() and ships the 128 bytes to the
+    other ranks; every rank then constructs Comm(uid, nranks, rank, device)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _ok(lib.ts_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        h = _vp()
+        _ok(lib.ts_comm_create(C.create_string_buffer(bytes(uid), 128), nranks, rank, device,
+                               C.byref(h)))
+        self._h = h
+        self.nranks, self.rank, self.device = nranks, rank, device
+
+    def close(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.ts_comm_destroy(self._h)
+        self._h = None
+
+    __del__ = close
 
 
 def _levels(levels):
@@ -338,6 +399,18 @@ class Operator:
         return cls(h)
 
     @classmethod
+    def split_multi(cls, bg: BlockGenerator, devices, precision=C128, storage=STORAGE_AUTO, s0=0j):
+        """One operator over several GPUs (ts_operator_create_split_multi):
+        branch partition, x broadcast and NCCL reduce inside the library."""
+        opt = TsSplitOptions()
+        lib.ts_split_options_default(C.byref(opt))
+        opt.precision, opt.storage, opt.s0_re, opt.s0_im = precision, storage, s0.real, s0.imag
+        devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+        h = _vp()
+        _ok(lib.ts_operator_create_split_multi(bg._h, C.byref(opt), len(devices), devs, C.byref(h)))
+        return cls(h)
+
+    @classmethod
     def load_split(cls, path):
         h = _vp()
         _ok(lib.ts_operator_load_split(os.fsencode(path), C.byref(h)))
@@ -369,12 +442,18 @@ class Operator:
         _ok(lib.ts_operator_save_kernel(self._h, os.fsencode(path)))
 
     # -- apply ---------------------------------------------------------------
-    def apply(self, v, policy=None, metrics=False):
-        """Host apply through ts_operator_apply (interleaved doubles)."""
+    def apply(self, v, policy=None, metrics=False, out=None):
+        """Host apply through ts_operator_apply (interleaved doubles). out: an
+        optional complex128 array to write y into (reused across calls)."""
         inf = self.info()
         count = int(np.prod(self.levels)) * inf["m"]
         va, vp = _cbuf(v, count)
-        y = np.zeros(count, np.complex128)
+        if out is None:
+            y = np.zeros(count, np.complex128)
+        else:
+            y = out
+            if y.dtype != np.complex128 or y.size != count or not y.flags.c_contiguous:
+                raise ValueError(f"out must be a contiguous complex128 array of {count} values")
         m = TsMetrics()
         pol = None
         if policy is not None:
@@ -383,12 +462,34 @@ class Operator:
                                   C.byref(pol) if pol is not None else None, C.byref(m)))
         return (y, m.as_dict()) if metrics else y
 
+    def _check_device(self, x, y, nrhs=1):
+        """x, y: contiguous device tensors of the operator's precision holding
+        nrhs * m * prod(levels) elements on the operator's device (raises
+        ValueError otherwise: the C ABI takes raw pointers)."""
+        import torch
+
+        inf = self.info()
+        want = torch.complex64 if inf["precision"] == C64 else torch.complex128
+        count = int(np.prod(self.levels)) * inf["m"] * int(nrhs)
+        for name, t in (("x", x), ("y", y)):
+            if not isinstance(t, torch.Tensor) or not t.is_cuda:
+                raise ValueError(f"{name} must be a CUDA tensor")
+            if t.device.index != inf["device"]:
+                raise ValueError(f"{name} is on cuda:{t.device.index}, the operator on cuda:{inf['device']}")
+            if t.dtype != want:
+                raise ValueError(f"{name} must be {want} for this operator, got {t.dtype}")
+            if not t.is_contiguous():
+                raise ValueError(f"{name} must be contiguous")
+            if t.numel() != count:
+                raise ValueError(f"{name} must hold {count} elements, got {t.numel()}")
+
     def apply_device(self, x, y, stream=None, metrics=False):
         """y = T x on device tensors (torch complex64/complex128, contiguous,
         m * prod(levels) elements). stream: torch.cuda.Stream or None
         (current stream)."""
         import torch
 
+        self._check_device(x, y)
         if stream is None:
             stream = torch.cuda.current_stream(x.device)
         m = TsMetrics()
@@ -401,6 +502,7 @@ class Operator:
         """nrhs vectors back to back in x (and y), each as for apply_device."""
         import torch
 
+        self._check_device(x, y, nrhs)
         if stream is None:
             stream = torch.cuda.current_stream(x.device)
         m = TsMetrics()
@@ -409,10 +511,26 @@ class Operator:
                                                C.c_void_p(stream.cuda_stream), C.byref(m)))
         return m.as_dict() if metrics else None
 
+    def apply_device_comm(self, comm: "Comm", x, y, root=0, bcast_x=True, stream=None,
+                          metrics=False):
+        """Collective apply of a partition operator (part = rank): x broadcast
+        from root, partials summed onto root's y (NCCL inside the library)."""
+        import torch
+
+        self._check_device(x, y)
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device)
+        m = TsMetrics()
+        _ok(lib.ts_operator_apply_device_comm(self._h, comm._h, C.c_void_p(x.data_ptr()),
+                                              C.c_void_p(y.data_ptr()), int(root), int(bool(bcast_x)),
+                                              C.c_void_p(stream.cuda_stream), C.byref(m)))
+        return m.as_dict() if metrics else None
+
     def profile_device(self, x, y, stream=None):
         """Per-launch device times (CUDA events) and algorithmic bytes."""
         import torch
 
+        self._check_device(x, y)
         if stream is None:
             stream = torch.cuda.current_stream(x.device)
         cap = 4096

@@ -9,7 +9,9 @@
 #include <sstream>
 #include <string>
 
+#include "engine.hpp"
 #include "host.hpp"
+#include "multi.hpp"
 #include "tsk_launch.h"
 
 using namespace tsb;
@@ -401,5 +403,69 @@ ts_status ts_operator_profile_device(const ts_operator* op, const void* x, void*
 }
 
 int32_t ts_device_count(void) { return device_count(); }
+
+ts_status ts_device_memory_stats(int32_t device, ts_memory_stats* out)
+{
+    return guarded([&] {
+        need(out != nullptr);
+        if (device < 0 || device >= device_count())
+            fail(TS_ERR_INVALID_ARGUMENT, "invalid device ordinal");
+        meter_stats(device, out);
+    });
+}
+
+ts_status ts_device_memory_reset_peak(int32_t device)
+{
+    return guarded([&] {
+        if (device < 0 || device >= device_count())
+            fail(TS_ERR_INVALID_ARGUMENT, "invalid device ordinal");
+        meter_reset_peak(device);
+    });
+}
+
+ts_status ts_operator_create_split_multi(const ts_block_generator* g, const ts_split_options* opt,
+                                         int32_t ndev, const int32_t* devices, ts_operator** out)
+{
+    return guarded([&] {
+        need(g && out && devices && ndev > 0);
+        ts_split_options o;
+        ts_split_options_default(&o);
+        if (opt)
+            o = *opt;
+        auto dev = create_split_multi(g->g, o, std::vector<int>(devices, devices + ndev));
+        *out = new ts_operator{OperatorHandle{std::move(dev)}};
+    });
+}
+
+ts_status ts_comm_unique_id(unsigned char out[128])
+{
+    return guarded([&] {
+        need(out != nullptr);
+        comm_unique_id(out);
+    });
+}
+
+ts_status ts_comm_create(const unsigned char id[128], int32_t nranks, int32_t rank, int32_t device,
+                         ts_comm** out)
+{
+    return guarded([&] {
+        need(id && out);
+        if (device < 0 || device >= device_count())
+            fail(TS_ERR_INVALID_ARGUMENT, "invalid device ordinal");
+        *out = reinterpret_cast<ts_comm*>(comm_create(id, nranks, rank, device));
+    });
+}
+
+void ts_comm_destroy(ts_comm* comm) { comm_destroy(reinterpret_cast<Comm*>(comm)); }
+
+ts_status ts_operator_apply_device_comm(const ts_operator* op, ts_comm* comm, const void* x, void* y,
+                                        int32_t root, int32_t bcast_x, void* stream, ts_metrics* metrics)
+{
+    return guarded([&] {
+        need(op && comm);
+        apply_device_comm(*op->h.dev, reinterpret_cast<Comm*>(comm), x, y, root, bcast_x,
+                          static_cast<cudaStream_t>(stream), metrics);
+    });
+}
 
 }  // extern "C"

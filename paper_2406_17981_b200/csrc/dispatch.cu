@@ -26,32 +26,25 @@ static bool env_flag(const char* name)
     const char* e = getenv(name);
     return e && e[0] == '1';
 }
+// A/B switches, read once (thread-safe static initialisation)
 static bool no_wide()
 {
-    static int v = -1;
-    if (v < 0)
-        v = env_flag("TSK_NO_WIDE") ? 1 : 0;
-    return v == 1;
+    static const bool v = env_flag("TSK_NO_WIDE");
+    return v;
 }
 
 // TSK_NO_LEAF1=1 selects the 3-components-per-thread leaf kernel (A/B).
 static bool no_leaf1()
 {
-    static int v = -1;
-    if (v < 0)
-        v = env_flag("TSK_NO_LEAF1") ? 1 : 0;
-    return v == 1;
+    static const bool v = env_flag("TSK_NO_LEAF1");
+    return v;
 }
 
 // TSK_GENERIC_ONLY=1 forces the generic kernels (tests cross-check the two).
 static bool generic_only()
 {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TSK_GENERIC_ONLY");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
+    static const bool v = env_flag("TSK_GENERIC_ONLY");
+    return v;
 }
 
 extern "C" int tsk_fwd_split(const tsk_axis* a, void* stream)
@@ -82,16 +75,39 @@ extern "C" int tsk_inv_merge(const tsk_axis* a, void* stream)
     return e == -1 ? tsk_global_inv_merge(a, stream) : e;
 }
 
-extern "C" int tsk_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream)
+static int leaf_one(const tsk_axis* a, const tsk_spectra* sp, void* stream)
 {
     if (!generic_only()) {
-        int e = no_leaf1() ? -1 : tsk_leaf1_pair(a, sp, stream);
-        if (e != -1)
-            return e;
-        e = tsk_fast_leaf_pair(a, sp, stream);
+        int e = tsk_fast_leaf_pair(a, sp, stream);
         if (e != -1)
             return e;
     }
     const int e = tsk_generic_leaf_pair(a, sp, stream);
     return e == -1 ? tsk_global_leaf_pair(a, sp, stream) : e;
+}
+
+// Batched leaf pass (a->nrhs right-hand sides): the leaf1 kernel runs all of
+// them in one launch (units of the same spectra row adjacent, so the row is
+// fetched from HBM once); the other kernels are launched per right-hand side.
+extern "C" int tsk_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream)
+{
+    if (!generic_only() && !no_leaf1()) {
+        const int e = tsk_leaf1_pair(a, sp, stream);
+        if (e != -1)
+            return e;
+    }
+    const int64_t nrhs = a->nrhs > 1 ? a->nrhs : 1;
+    if (nrhs == 1)
+        return leaf_one(a, sp, stream);
+    const size_t es = a->prec ? 8 : 16;
+    for (int64_t r = 0; r < nrhs; ++r) {
+        tsk_axis one = *a;
+        one.nrhs = 1;
+        one.src0 = static_cast<const char*>(a->src0) + static_cast<size_t>(r * a->rstride) * es;
+        one.dst0 = static_cast<char*>(a->dst0) + static_cast<size_t>(r * a->rstride) * es;
+        const int e = leaf_one(&one, sp, stream);
+        if (e != 0)
+            return e;
+    }
+    return 0;
 }

@@ -405,10 +405,14 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     };
     const uint32_t mask1 = A1 >= 0 ? axis_mask(A1) : 0u, mask2 = A2 >= 0 ? axis_mask(A2) : 0u;
     const FastDiv div2((uint32_t)st2), div1((uint32_t)st1);
-    // compressed: one unit = one mirror orbit; full storage: 4 consecutive fibers
-    const int64_t units = CMP ? rest * st1 * st2 : (p.outer + 3) / 4;
-    const T2* src = static_cast<const T2*>(p.src0);
-    T2* dst = static_cast<T2*>(p.dst0);
+    // compressed: one unit = one mirror orbit; full storage: 4 consecutive
+    // fibers; times nrhs right-hand sides, the RHS index fastest so that the
+    // units sharing a spectra row run side by side (one HBM fetch per row)
+    const int64_t nrhs = p.nrhs > 1 ? p.nrhs : 1;
+    const FastDiv divr((uint32_t)nrhs);
+    const int64_t units = (CMP ? rest * st1 * st2 : (p.outer + 3) / 4) * nrhs;
+    const T2* src0 = static_cast<const T2*>(p.src0);
+    T2* dst0 = static_cast<T2*>(p.dst0);
     const T2* spec = static_cast<const T2*>(sp.data);
     T2 ekeep[TM ? 1 : R];
 
@@ -417,6 +421,15 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
         const bool uvalid = u < units;
         if (!uvalid)
             u = units - 1;  // runs in lockstep (barriers), stores nothing
+        const T2* src = src0;
+        T2* dst = dst0;
+        if (nrhs > 1) {  // units < 2^31 (checked by the launcher)
+            const uint32_t ur = divr.div((uint32_t)u);
+            const int64_t r = u - (int64_t)ur * nrhs;
+            src += r * p.rstride;
+            dst += r * p.rstride;
+            u = ur;
+        }
         // ---- unit geometry: fiber g of orbit member f, spectra row offsets,
         // signs. Members past the orbit size alias a real member (loads stay in
         // range) and skip the store.
@@ -774,6 +787,9 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
     } else {
         units = (a.outer + 3) / 4;
     }
+    units *= a.nrhs > 1 ? a.nrhs : 1;
+    if (units >= (int64_t(1) << 31))
+        return -1;
     const int64_t tiles = (units + G - 1) / G;
     const int64_t grid = tiles < cap ? tiles : cap;
     kern<<<(unsigned)(grid > 0 ? grid : 1), NT, smem, st>>>(a, sp);

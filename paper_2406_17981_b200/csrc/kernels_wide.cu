@@ -352,11 +352,10 @@ static int launch(const tsk_axis& a, cudaStream_t st)
 // K3 1.92 -> 1.88 ms). TSK_WIDE_SEG=128|256 overrides both (A/B).
 static int seg_bytes(int mode, int64_t stride_bytes)
 {
-    static int v = -1;
-    if (v < 0) {
+    static const int v = [] {
         const char* e = getenv("TSK_WIDE_SEG");
-        v = e ? atoi(e) : 0;
-    }
+        return e ? atoi(e) : 0;
+    }();
     if (v == 128 || v == 256)
         return v;
     (void)mode;

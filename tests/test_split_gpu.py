@@ -303,15 +303,64 @@ def test_partitions_fast_path_dyadic(nparts, prec, tol):
     assert rel_l2(acc, ys) <= tol
 
 
-@pytest.mark.parametrize("levels", [[32, 32, 32], [16, 8, 64], [64, 16, 8]])
-def test_fast_and_generic_agree(levels, monkeypatch):
-    # TSK_GENERIC_ONLY is read once per process, so compare against the oracle
-    # on shapes that route through the fast kernels
-    for sym in SYM:
+_SUBPROC = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2406_17981_b200 as T
+cases = {cases!r}
+out = {{}}
+for i, (levels, sym, prec, dyadic) in enumerate(cases):
+    if dyadic:
+        import oracle
+        s = int(np.prod(levels))
+        x = oracle.Oracle().random_vector([3] + levels, 19, 0.5)
+        op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec)
+    else:
         g = T.Generator.random(levels, 13, 1.0, sym)
-        lags, v, y_or = _oracle_split(levels, sym, 13)
-        y = T.Operator.split(g).apply(v)
-        assert rel_l2(y, y_or) <= 1e-12
+        x = T.random_vector(levels, 13, 1.0)
+        op = T.Operator.split_ex(T.BlockGenerator.from_scalar(g), precision=prec)
+    out[str(i)] = op.apply(x)
+np.savez({path!r}, **out)
+"""
+
+
+def _run_with_env(env_var, cases):
+    """y for each case computed in a fresh process with env_var=1 (the
+    kernel-selection switches are read once per process)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "y.npz")
+        env = dict(os.environ, **{env_var: "1"})
+        r = subprocess.run([sys.executable, "-c", _SUBPROC.format(root=root, cases=cases, path=path)],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        z = np.load(path)
+        return [z[str(i)] for i in range(len(cases))]
+
+
+def test_fast_and_generic_agree():
+    # TSK_GENERIC_ONLY=1 (fresh process) forces the generic mixed-radix kernels
+    # on shapes the fast/wide/leaf kernels otherwise take; both against the oracle
+    cases = [([32, 32, 32], T.SYM_GENERAL, T.C128, False), ([16, 8, 64], T.SYM_SYMMETRIC, T.C128, False),
+             ([64, 16, 8], T.SYM_SKEW, T.C128, False), ([8, 16, 128], 0, T.C64, True)]
+    gen = _run_with_env("TSK_GENERIC_ONLY", cases)
+    for (levels, sym, prec, dyadic), yg in zip(cases, gen):
+        if dyadic:
+            xs = _dyadic_x(levels, 19)
+            y_or = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+            y = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec).apply(np.concatenate(xs))
+            tol = 1e-5
+        else:
+            g = T.Generator.random(levels, 13, 1.0, sym)
+            _, v, y_or = _oracle_split(levels, sym, 13)
+            y = T.Operator.split(g).apply(v)
+            tol = 1e-12
+        assert rel_l2(yg, y_or) <= tol
+        assert rel_l2(y, y_or) <= tol
+        assert rel_l2(yg, y) <= 2 * tol
 
 
 @pytest.mark.parametrize("levels", [[512, 8, 32], [256, 32, 16], [128, 64, 32], [64, 64, 64],
@@ -399,14 +448,24 @@ def test_leaf_kernel_partitions(nparts, n):
     assert rel_l2(acc, ys) <= 1e-5
 
 
-def test_leaf_kernel_matches_previous_leaf_kernel(monkeypatch):
-    # the 8-point leaf kernel (TSK_NO_LEAF1=1 in a fresh process) is the A/B
-    # partner; here both must agree with the oracle on the same operator
-    levels = [3, 4, 128]
-    xs = _dyadic_x(levels, 19)
-    ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
-    op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=T.C64)
-    assert rel_l2(op.apply(np.concatenate(xs)), ys) <= 1e-5
+def test_leaf_kernel_matches_previous_leaf_kernel():
+    # the 8-point leaf kernel (k_leaf, TSK_NO_LEAF1=1 in a fresh process) is
+    # the A/B partner of k_leaf1; both against the oracle and each other
+    cases = [([3, 4, 128], 0, T.C64, True), ([4, 4, 512], 0, T.C64, True),
+             ([2, 8, 256], T.SYM_SYMMETRIC, T.C64, False)]
+    prev = _run_with_env("TSK_NO_LEAF1", cases)
+    for (levels, sym, prec, dyadic), yp in zip(cases, prev):
+        if dyadic:
+            xs = _dyadic_x(levels, 19)
+            y_or = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+            y = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec).apply(np.concatenate(xs))
+        else:
+            g = T.Generator.random(levels, 13, 1.0, sym)
+            _, v, y_or = _oracle_split(levels, sym, 13)
+            y = T.Operator.split_ex(T.BlockGenerator.from_scalar(g), precision=prec).apply(v)
+        assert rel_l2(yp, y_or) <= 1e-5
+        assert rel_l2(y, y_or) <= 1e-5
+        assert rel_l2(yp, y) <= 1e-5
 
 
 # ---- long axes: fibers too long to stage in shared memory run the global-
