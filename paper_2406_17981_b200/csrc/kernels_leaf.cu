@@ -410,6 +410,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     const uint32_t gmask = SF ? sp.skew_mask[sp.comp_map[0]] : 0u;
     const uint32_t cmask = SF ? (sp.skew_mask[sp.comp_map[c]] ^ gmask) : 0u;
     const uint32_t zlast = (cmask >> (d - 1)) & 1u, glast = (gmask >> (d - 1)) & 1u;
+
     // compressed: one unit = one mirror orbit; full storage: 4 consecutive
     // fibers; times nrhs right-hand sides, the RHS index fastest so that the
     // units sharing a spectra row run side by side (one HBM fetch per row)
@@ -502,14 +503,16 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
         // component c flips its transform by cpar_c(F(k)) (wlo / whi by half),
         // the reader's gpar cpar_C is a per-fiber constant folded into the
         // output scale plus a half flip (hsg) on the mirrored half
-        T wlo = (T)1, whi = (T)1, hsg = (T)1;
+        // (sign bits: the flips run as XORs on the integer pipe; the FP32
+        // pipe is one of the pass's two limiters)
+        uint32_t wlo = 0, whi = 0, hsg = 0;
         if constexpr (SF && CMP) {
             const uint32_t fz = (uint32_t)__popc(fax & cmask) & 1u, fg = (uint32_t)__popc(fax & gmask) & 1u;
-            wlo = fz ? (T)-1 : (T)1;
-            whi = (fz ^ zlast) ? (T)-1 : (T)1;
+            wlo = fz;
+            whi = fz ^ zlast;
             scale = (fz ^ fg) ? -scale0 : scale0;
             pts = twv<T>(make_c<T>(pt.lo.x * scale, pt.lo.y * scale));
-            hsg = (glast ^ zlast) ? (T)-1 : (T)1;
+            hsg = glast ^ zlast;
         }
         // sign masks per unique component: bit uu of neg (unmirrored k) and
         // of neg ^ lastneg (mirrored k)
@@ -575,7 +578,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
 #pragma unroll
                 for (int m = 0; m < R; ++m) {
                     const bool mir = 2 * m > R || (2 * m == R && (beta == 1 || t != 0));
-                    v[m] = scale_c<T>(v[m], 2 * m < R ? wlo : (2 * m > R ? whi : (mir ? whi : wlo)));
+                    v[m] = flip_bits<T>(v[m], 2 * m < R ? wlo : (2 * m > R ? whi : (mir ? whi : wlo)));
                 }
             }
 
@@ -655,9 +658,9 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                     });
                     if constexpr (SF && CMP) {
                         if (2 * m > R)
-                            acc = scale_c<T>(acc, hsg);
+                            acc = flip_bits<T>(acc, hsg);
                         else if (2 * m == R)
-                            acc = scale_c<T>(acc, (beta == 1 || t != 0) ? hsg : (T)1);
+                            acc = flip_bits<T>(acc, (beta == 1 || t != 0) ? hsg : 0u);
                     }
                     v[m] = acc;
                     if (m % 2 == 1)
