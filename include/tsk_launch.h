@@ -89,6 +89,14 @@ int tsk_embed_generator(int32_t d, const int64_t* levels, const void* lags, doub
 int tsk_embed_dyadic(int32_t d, const int64_t* levels, int32_t i, int32_t j, double k,
                      double self_re, double self_im, double s0_re, double s0_im, void* out,
                      void* stream);
+/* Embedding + first branchwise fold along axis 0 in one sweep (the (2n)^d
+ * embedding is never materialised): out (n_0 x 2n_1 x ... x 2n_{d-1}, c128)
+ * = lo + hi (odd = 0) or e^{-i pi k/n_0} (lo - hi) (odd = 1). Source: the lag
+ * tensor `lags` (as tsk_embed_generator), or with lags == NULL the analytic
+ * dyadic G_ij (as tsk_embed_dyadic). Bit-identical to embed + fold_axis. */
+int tsk_embed_fold0(int32_t d, const int64_t* levels, const void* lags, int32_t dyadic_i, int32_t dyadic_j,
+                    double k, double self_re, double self_im, double s0_re, double s0_im, int32_t odd,
+                    void* out, void* stream);
 /* kernel.cpp:223-258 fold along `axis` of a tensor of shape `shape` (c128):
  * even = lo + hi, odd = e^{-i pi k/n} (lo - hi); out has shape[axis]/2. */
 int tsk_fold_axis(int32_t d, const int64_t* shape, int32_t axis, int32_t odd, const void* in,

@@ -50,7 +50,7 @@ EXTENSION_SYMBOLS = [
 LAUNCHER_SYMBOLS = [
     "tsk_fwd_split", "tsk_inv_merge", "tsk_leaf_pair", "tsk_embed_generator", "tsk_embed_dyadic",
     "tsk_fold_axis", "tsk_mirror_check", "tsk_store_block", "tsk_convert", "tsk_embed_corner",
-    "tsk_symbol_multiply",
+    "tsk_symbol_multiply", "tsk_embed_fold0",
 ]
 
 

@@ -327,31 +327,35 @@ std::shared_ptr<DeviceOperator> create_split(const BlockGenerator& g, const ts_s
         tmp.prec = 0;
         fill_tables(tmp, op->levels, pc.tabs64);
     }
-    Shape eshape(d);
+    // embedding + first fold in one sweep per (component, axis-0 parity): the
+    // (2n)^d embedding is never materialised (setup peak: the half tensor)
+    Shape half(d);
     for (int a = 0; a < d; ++a)
-        eshape[a] = 2 * g.levels[a];
-    const int64_t evol = volume(eshape);
-    DevBuf emb(static_cast<size_t>(evol) * 16, MEM_STAGING);
+        half[a] = 2 * g.levels[a];
+    half[0] = g.levels[0];
+    DevBuf h0(static_cast<size_t>(volume(half)) * 16, MEM_STAGING);
     DevBuf lagbuf;
     for (int u = 0; u < g.n_unique; ++u) {
         pc.u = u;
-        if (g.dyadic) {
-            launch_check(tsk_embed_dyadic(d, g.levels.data(), g.dyadic_ij[u].first,
-                                          g.dyadic_ij[u].second, g.k, g.self_term.real(),
-                                          g.self_term.imag(), s0.real(), s0.imag(), emb.p, st),
-                         "embed dyadic");
-        } else {
+        if (!g.dyadic) {
             const auto& lags = g.lags[u];
             if (!lagbuf.p)
                 lagbuf = DevBuf(lags.size() * 16, MEM_STAGING);
             cuda_check(cudaMemcpyAsync(lagbuf.p, lags.data(), lags.size() * 16,
                                        cudaMemcpyHostToDevice, st),
                        "upload lags");
-            launch_check(tsk_embed_generator(d, g.levels.data(), lagbuf.p, s0.real(), s0.imag(),
-                                             emb.p, st),
-                         "embed generator");
         }
-        pc.recurse(emb.p, eshape, 0, 0);
+        for (int odd = 0; odd < 2; ++odd) {
+            if (op->q > 0 && (op->part & 1) != odd)
+                continue;  // axis 0's other parity belongs to another partition
+            launch_check(tsk_embed_fold0(d, g.levels.data(), g.dyadic ? nullptr : lagbuf.p,
+                                         g.dyadic ? g.dyadic_ij[u].first : 0,
+                                         g.dyadic ? g.dyadic_ij[u].second : 0, g.k,
+                                         g.self_term.real(), g.self_term.imag(), s0.real(), s0.imag(),
+                                         odd, h0.p, st),
+                         "embed + fold");
+            pc.recurse(h0.p, half, 1, static_cast<uint32_t>(odd));
+        }
     }
     cuda_check(cudaStreamSynchronize(st), "precompute sync");
     op->precompute_ns = static_cast<uint64_t>(

@@ -46,11 +46,14 @@ static unsigned grid1d(int64_t total)
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (total); \
          i += (int64_t)gridDim.x * blockDim.x)
 
-// embedded column: per axis j < n -> lag j, j == n -> s0, j > n -> lag j-2n
-__global__ void k_embed_generator(Shape32 lv, const double2* __restrict__ lags, double2 s0,
-                                  double2* __restrict__ out, int64_t total)
-{
-    GRID_STRIDE(off, total)
+// Value of the embedded first column at embedded index off of the (2n)^d
+// layout: per axis j < n -> lag j, j == n -> s0 (padding), j > n -> lag j-2n
+// (ref kernel.cpp:50-82). Two sources: an explicit lag tensor and the
+// analytic dyadic G of BASELINE.json configs[1].
+struct LagSource {
+    const double2* __restrict__ lags;
+    double2 s0;
+    __device__ __forceinline__ double2 at(const Shape32& lv, int64_t off) const
     {
         int64_t rem = off;
         int64_t lag_off = 0, lag_stride = 1;
@@ -65,16 +68,17 @@ __global__ void k_embed_generator(Shape32 lv, const double2* __restrict__ lags, 
             lag_off += (m + n - 1) * lag_stride;
             lag_stride *= 2 * n - 1;
         }
-        out[off] = pad ? s0 : lags[lag_off];
+        return pad ? s0 : lags[lag_off];
     }
-}
+};
 
-// BASELINE.json configs[1] dyadic Green kernel evaluated at the embedded
-// positions (same formula as oracle/toesplit_oracle.c:orc_dyadic_lags).
-__global__ void k_embed_dyadic(Shape32 lv, int ci, int cj, double k, double2 self, double2 s0,
-                               double2* __restrict__ out, int64_t total)
-{
-    GRID_STRIDE(off, total)
+// same formula as oracle/toesplit_oracle.c:orc_dyadic_lags (rh_i rh_j formed
+// as m_i m_j / r^2, so mirrored lags are bit-exact)
+struct DyadicSource {
+    int ci, cj;
+    double k;
+    double2 self, s0;
+    __device__ __forceinline__ double2 at(const Shape32& lv, int64_t off) const
     {
         int64_t rem = off;
         bool pad = false;
@@ -108,11 +112,54 @@ __global__ void k_embed_dyadic(Shape32 lv, int ci, int cj, double k, double2 sel
             v.x = amp * c;
             v.y = amp * s;
         }
-        out[off] = v;
+        return v;
+    }
+};
+
+template <class Src>
+__global__ void k_embed(Shape32 lv, Src src, double2* __restrict__ out, int64_t total)
+{
+    GRID_STRIDE(off, total)
+    out[off] = src.at(lv, off);
+}
+
+// Embedding and the first branchwise fold (axis 0, ref kernel.cpp:223-258)
+// in one sweep: out[k0, ...] = lo + hi (even) or e^{-i pi k0/n0} (lo - hi)
+// (odd) with lo / hi the embedded values at k0 and k0 + n0, evaluated on the
+// fly — the (2n)^d embedding is never materialised (half the setup memory).
+// Same operations in the same order as k_embed + k_fold_axis: bit-identical.
+template <class Src>
+__global__ void k_embed_fold0(Shape32 lv, Src src, int odd, double2* __restrict__ out, int64_t total_out)
+{
+    const int64_t n = lv.n[0];
+    int64_t inner = 1;
+    for (int a = 1; a < lv.d; ++a)
+        inner *= 2 * lv.n[a];
+    GRID_STRIDE(off, total_out)
+    {
+        const int64_t i = off % inner;
+        const int64_t k = off / inner;
+        const double2 lo = src.at(lv, k * inner + i);
+        const double2 hi = src.at(lv, (n + k) * inner + i);
+        double2 r;
+        if (odd) {
+            double s, c;
+            sincospi(-(double)k / (double)n, &s, &c);
+            double2 dd;
+            dd.x = lo.x - hi.x;
+            dd.y = lo.y - hi.y;
+            double2 f;
+            f.x = c;
+            f.y = s;
+            r = cmul(f, dd);
+        } else {
+            r.x = lo.x + hi.x;
+            r.y = lo.y + hi.y;
+        }
+        out[off] = r;
     }
 }
 
-// r2 accumulates over axes in reverse order in the kernel above; squares of
 // small integers are exact, so the sum is order independent.
 
 __global__ void k_fold_axis(Shape32 in_shape, int axis, int odd, const double2* __restrict__ in,
@@ -304,11 +351,9 @@ int tsk_embed_generator(int32_t d, const int64_t* levels, const void* lags, doub
                         double s0_im, void* out, void* stream)
 {
     Shape32 lv = make_shape(d, levels);
-    int64_t total = 1;
-    for (int a = 0; a < d; ++a)
-        total *= 2 * levels[a];
-    k_embed_generator<<<grid1d(total), 256, 0, (cudaStream_t)stream>>>(
-        lv, (const double2*)lags, make_double2(s0_re, s0_im), (double2*)out, total);
+    const int64_t total = vol(lv) << d;
+    k_embed<<<grid1d(total), 256, 0, (cudaStream_t)stream>>>(
+        lv, LagSource{(const double2*)lags, make_double2(s0_re, s0_im)}, (double2*)out, total);
     return (int)cudaGetLastError();
 }
 
@@ -317,12 +362,27 @@ int tsk_embed_dyadic(int32_t d, const int64_t* levels, int32_t i, int32_t j, dou
                      void* stream)
 {
     Shape32 lv = make_shape(d, levels);
-    int64_t total = 1;
-    for (int a = 0; a < d; ++a)
-        total *= 2 * levels[a];
-    k_embed_dyadic<<<grid1d(total), 256, 0, (cudaStream_t)stream>>>(
-        lv, i, j, k, make_double2(self_re, self_im), make_double2(s0_re, s0_im), (double2*)out,
-        total);
+    const int64_t total = vol(lv) << d;
+    k_embed<<<grid1d(total), 256, 0, (cudaStream_t)stream>>>(
+        lv, DyadicSource{i, j, k, make_double2(self_re, self_im), make_double2(s0_re, s0_im)},
+        (double2*)out, total);
+    return (int)cudaGetLastError();
+}
+
+int tsk_embed_fold0(int32_t d, const int64_t* levels, const void* lags, int32_t dyadic_i, int32_t dyadic_j,
+                    double k, double self_re, double self_im, double s0_re, double s0_im, int32_t odd,
+                    void* out, void* stream)
+{
+    Shape32 lv = make_shape(d, levels);
+    const int64_t total_out = vol(lv) << (d - 1);
+    const double2 s0 = make_double2(s0_re, s0_im);
+    if (lags)
+        k_embed_fold0<<<grid1d(total_out), 256, 0, (cudaStream_t)stream>>>(
+            lv, LagSource{(const double2*)lags, s0}, odd, (double2*)out, total_out);
+    else
+        k_embed_fold0<<<grid1d(total_out), 256, 0, (cudaStream_t)stream>>>(
+            lv, DyadicSource{dyadic_i, dyadic_j, k, make_double2(self_re, self_im), s0}, odd,
+            (double2*)out, total_out);
     return (int)cudaGetLastError();
 }
 

@@ -269,7 +269,7 @@ constexpr int leaf1_g()
     return 128 / gcd_i(128, 4 * M * (N / R));
 }
 
-template <typename T, int N, int R, int M, bool CMP, bool SF, int G = leaf1_g<N, R, M>()>
+template <typename T, int N, int R, int M, bool CMP, int G = leaf1_g<N, R, M>()>
 // 16 elements per thread fit two 384-thread CTAs per SM (80 registers, 24
 // warps): the 256-point leaf 0.41 -> 0.365 ms at 256^3
 #ifndef TSK_LEAF256_2CTA
@@ -314,9 +314,8 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     const Tw<T> pt = twv<T>(ldg_c(static_cast<const T2*>(p.phase) + t));
     // output scale 1/(2n) folded into the odd branch's conj phase and the
     // merge FMA (the spectra multiply only flips signs)
-    const T scale0 = (T)p.scale;
-    T scale = scale0;
-    Tw<T> pts = twv<T>(make_c<T>(pt.lo.x * scale, pt.lo.y * scale));
+    const T scale = (T)p.scale;
+    const Tw<T> pts = twv<T>(make_c<T>(pt.lo.x * scale, pt.lo.y * scale));
 
     // e' parked in TMEM when it is a multiple of 32 words, else in registers
     constexpr int EW = R * (int)sizeof(T2) / 4;
@@ -406,11 +405,6 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     };
     const uint32_t mask1 = A1 >= 0 ? axis_mask(A1) : 0u, mask2 = A2 >= 0 ? axis_mask(A2) : 0u;
     const FastDiv div2((uint32_t)st2), div1((uint32_t)st1);
-    // SF: per-component axis masks of the factorised skew signs (host-checked)
-    const uint32_t gmask = SF ? sp.skew_mask[sp.comp_map[0]] : 0u;
-    const uint32_t cmask = SF ? (sp.skew_mask[sp.comp_map[c]] ^ gmask) : 0u;
-    const uint32_t zlast = (cmask >> (d - 1)) & 1u, glast = (gmask >> (d - 1)) & 1u;
-
     // compressed: one unit = one mirror orbit; full storage: 4 consecutive
     // fibers; times nrhs right-hand sides, the RHS index fastest so that the
     // units sharing a spectra row run side by side (one HBM fetch per row)
@@ -440,9 +434,8 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
         // signs. Members past the orbit size alias a real member (loads stay in
         // range) and skip the store.
         auto geometry = [&](int64_t u, bool uvalid, bool& valid, int64_t& g, int64_t& off0, int64_t& off1,
-                            uint32_t& neg, uint32_t& fax) {
+                            uint32_t& neg) {
             neg = 0;
-            fax = 0;
             if constexpr (!CMP) {
                 g = u * 4 + f;
                 valid = uvalid && g < p.outer;
@@ -462,14 +455,10 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 const int i1 = c2 == 2 ? (f >> 1) & (c1 - 1) : f & (c1 - 1), i2 = f & (c2 - 1);
                 const int64_t kk1 = A1 < 0 ? 0 : (i1 ? p1 : s1);
                 const int64_t kk2 = A2 < 0 ? 0 : (i2 ? p2 : s2);
-                if (i1) {
+                if (i1)
                     neg ^= mask1;
-                    fax |= 1u << A1;
-                }
-                if (i2) {
+                if (i2)
                     neg ^= mask2;
-                    fax |= 1u << A2;
-                }
                 int64_t rsrc = 0, rstr = 1, gr = r, rfull = 0, rmul = 1;
                 for (int a = A1 - 1; a >= 0; --a) {
                     const int64_t na = sp.levels[a];
@@ -481,12 +470,9 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                     rstr *= stored_len(na, odd);
                     rfull += ka * rmul;
                     rmul *= na;
-                    if (mm) {
-                        fax |= 1u << a;
-                        if constexpr (!SF)
-                            for (int uu = 0; uu < U; ++uu)
-                                neg ^= ((sp.skew_mask[uu] >> a) & 1u) << uu;
-                    }
+                    if (mm)
+                        for (int uu = 0; uu < U; ++uu)
+                            neg ^= ((sp.skew_mask[uu] >> a) & 1u) << uu;
                 }
                 g = (rfull * n1 + kk1) * n2 + kk2;
                 const int64_t row = (rsrc * st1 + s1) * st2 + s2;
@@ -496,24 +482,8 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
         };
         bool valid;
         int64_t g, off0, off1;
-        uint32_t neg, fax;
-        geometry(u, uvalid, valid, g, off0, off1, neg, fax);
-        // SF (factorised signs): the mirror sign of unique component (i, j)
-        // under mirrored axes F is gpar(F) cpar_i(F) cpar_j(F); the writer of
-        // component c flips its transform by cpar_c(F(k)) (wlo / whi by half),
-        // the reader's gpar cpar_C is a per-fiber constant folded into the
-        // output scale plus a half flip (hsg) on the mirrored half
-        // (sign bits: the flips run as XORs on the integer pipe; the FP32
-        // pipe is one of the pass's two limiters)
-        uint32_t wlo = 0, whi = 0, hsg = 0;
-        if constexpr (SF && CMP) {
-            const uint32_t fz = (uint32_t)__popc(fax & cmask) & 1u, fg = (uint32_t)__popc(fax & gmask) & 1u;
-            wlo = fz;
-            whi = fz ^ zlast;
-            scale = (fz ^ fg) ? -scale0 : scale0;
-            pts = twv<T>(make_c<T>(pt.lo.x * scale, pt.lo.y * scale));
-            hsg = glast ^ zlast;
-        }
+        uint32_t neg;
+        geometry(u, uvalid, valid, g, off0, off1, neg);
         // sign masks per unique component: bit uu of neg (unmirrored k) and
         // of neg ^ lastneg (mirrored k)
         const uint32_t neg0 = neg, neg1 = neg ^ lastneg;
@@ -574,13 +544,6 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 }
             }
             fft_one<T, N, R, false, TWT>(v, buf, tw, t, quad + TWOFF);
-            if constexpr (SF && CMP && M > 1) {
-#pragma unroll
-                for (int m = 0; m < R; ++m) {
-                    const bool mir = 2 * m > R || (2 * m == R && (beta == 1 || t != 0));
-                    v[m] = flip_bits<T>(v[m], 2 * m < R ? wlo : (2 * m > R ? whi : (mir ? whi : wlo)));
-                }
-            }
 
             // ---- spectra multiply y_c = sum_c' T_{c c'} x_c' (components meet in smem)
             if constexpr (MIXT) {
@@ -640,9 +603,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                         else
                             ng = neg1;
                         T2 s_;
-                        if constexpr (CMP && SF)
-                            s_ = sp_[uu * LROW];
-                        else if constexpr (CMP)
+                        if constexpr (CMP)
                             s_ = flip_bits<T>(sp_[uu * LROW], (ng >> uu) & 1u);
                         else  // full storage: this fiber's own row, read once
                             s_ = ldg_c(spec + sp.branch_base[beta] + (beta ? off1 : off0) +
@@ -656,12 +617,6 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                             xv = fbufs[(f * M + cc) * NP + Pad<N, R>::rd(t, m)];
                         acc = cmac<T>(acc, xv, s_, cc == 0);
                     });
-                    if constexpr (SF && CMP) {
-                        if (2 * m > R)
-                            acc = flip_bits<T>(acc, hsg);
-                        else if (2 * m == R)
-                            acc = flip_bits<T>(acc, (beta == 1 || t != 0) ? hsg : 0u);
-                    }
                     v[m] = acc;
                     if (m % 2 == 1)
                         asm volatile("" ::: "memory");  // bound the loads in flight
@@ -781,7 +736,7 @@ static int sm_count()
     return sms > 0 ? sms : 148;
 }
 
-template <typename T, int N, int R, int M, bool CMP, bool SF>
+template <typename T, int N, int R, int M, bool CMP>
 static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
     using T2 = typename cx<T>::t;
@@ -793,7 +748,7 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         sizeof(T2) * (R * (N / R - 1) + G * 4 * M * NP + G * (M == 1 ? 1 : 6) * (N / 2 + 1));
     if (smem > 227 * 1024)
         return -1;
-    auto kern = k_leaf1<T, N, R, M, CMP, SF>;
+    auto kern = k_leaf1<T, N, R, M, CMP>;
     static thread_local int cached_dev = -1, cap = 0;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -816,8 +771,8 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         if (getenv("TSK_DEBUG_OCC")) {
             cudaFuncAttributes fa{};
             cudaFuncGetAttributes(&fa, kern);
-            fprintf(stderr, "k_leaf1<%d,%d,%d,%d,%d,%d>: %d CTAs/SM, %zu B smem (+%zu static), %d threads, %d regs\n",
-                    (int)sizeof(T), N, R, M, (int)CMP, (int)SF, per_sm, smem, fa.sharedSizeBytes, NT, fa.numRegs);
+            fprintf(stderr, "k_leaf1<%d,%d,%d,%d,%d>: %d CTAs/SM, %zu B smem (+%zu static), %d threads, %d regs\n",
+                    (int)sizeof(T), N, R, M, (int)CMP, per_sm, smem, fa.sharedSizeBytes, NT, fa.numRegs);
         }
         cap = sm_count() * (per_sm > 0 ? per_sm : 1);
         cached_dev = dev;
@@ -841,48 +796,23 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
     return (int)cudaGetLastError();
 }
 
-template <typename T, int M, bool CMP, bool SF>
+template <typename T, int M, bool CMP>
 static int dispatch_s(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
     switch (a.n) {
-    case 64: return launch<T, 64, 8, M, CMP, SF>(a, sp, st);
-    case 128: return launch<T, 128, 16, M, CMP, SF>(a, sp, st);
-    case 256: return launch<T, 256, 16, M, CMP, SF>(a, sp, st);
+    case 64: return launch<T, 64, 8, M, CMP>(a, sp, st);
+    case 128: return launch<T, 128, 16, M, CMP>(a, sp, st);
+    case 256: return launch<T, 256, 16, M, CMP>(a, sp, st);
     case 512:  // complex128 at R = 32 spills; the 8-point kernel handles it
-        return sizeof(T) == 4 ? launch<T, 512, 32, M, CMP, SF>(a, sp, st) : -1;
+        return sizeof(T) == 4 ? launch<T, 512, 32, M, CMP>(a, sp, st) : -1;
     default: return -1;
     }
-}
-
-// The mirror signs factorise when skew(i, j) = g ^ c_i ^ c_j (axis masks) for
-// every block position: the dyadic G (c_i = axis i, g = 0) and every scalar
-// generator (c_0 = 0, g = its skew mask). TSK_LEAF_NO_SF=1: per-value flips (A/B).
-static bool signs_factorise(const tsk_spectra& sp)
-{
-    static const bool off = [] {
-        const char* e = getenv("TSK_LEAF_NO_SF");
-        return e && e[0] == '1';
-    }();
-    if (off || !sp.compressed)
-        return false;
-    const int m = sp.m;
-    const uint32_t g = sp.skew_mask[sp.comp_map[0]];
-    for (int i = 0; i < m; ++i)
-        for (int j = 0; j < m; ++j) {
-            const uint32_t ci = sp.skew_mask[sp.comp_map[i]] ^ g, cj = sp.skew_mask[sp.comp_map[j]] ^ g;
-            if (sp.skew_mask[sp.comp_map[i * m + j]] != (g ^ ci ^ cj))
-                return false;
-        }
-    return true;
 }
 
 template <typename T, int M>
 static int dispatch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
-    if (!sp.compressed)
-        return dispatch_s<T, M, false, false>(a, sp, st);
-    return signs_factorise(sp) ? dispatch_s<T, M, true, true>(a, sp, st)
-                               : dispatch_s<T, M, true, false>(a, sp, st);
+    return sp.compressed ? dispatch_s<T, M, true>(a, sp, st) : dispatch_s<T, M, false>(a, sp, st);
 }
 
 }  // namespace leaf

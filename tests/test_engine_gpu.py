@@ -124,8 +124,13 @@ def test_memory_meter_counts_library_buffers():
     assert inf["cached_bytes"] == inf["workspace_bytes"] == 2 * x.numel() * 8  # (d-1) children
     assert st["live_bytes"] - before["live_bytes"] == inf["spectra_bytes"] + inf["table_bytes"] + inf["cached_bytes"]
     assert st["peak_bytes"] >= st["live_bytes"]
-    # the precompute's staging (the (2n)^3 complex128 embedding) is in the peak
-    assert st["peak_bytes"] - before["live_bytes"] >= 8 * int(np.prod(levels)) * 16
+    # the precompute's staging is in the peak: the embedded-and-folded half
+    # tensor (4 s complex128; the (2n)^3 embedding itself is never stored)
+    # plus the deeper fold levels, next to the spectra
+    s = int(np.prod(levels))
+    peak_setup = st["peak_bytes"] - before["live_bytes"]
+    assert peak_setup >= inf["spectra_bytes"] + 4 * s * 16
+    assert peak_setup < inf["spectra_bytes"] + 8 * s * 16
     del op
     assert T.memory_stats(0)["live_bytes"] == before["live_bytes"]
 
