@@ -1,4 +1,4 @@
-"""World-size-2 (and 4) CPU tests of the multi-GPU path's host logic with the
+"""World-size-2 (and 4) tests of the multi-GPU path's host logic with the
 gloo backend: each rank owns the branch subtree of partition.owned_branches,
 computes its projected partial output (here with the CPU oracle — the GPU
 ranks do it with ts_operator_create_split_ex(part, nparts)), and
@@ -82,3 +82,47 @@ def test_partition_logic():
     # SURVEY.md §8(e) per-GPU vector traffic table
     assert [partition.per_gpu_vector_passes(3, p) for p in (1, 2, 4, 8)] == [26, 14, 10, 10]
     assert [partition.per_gpu_vector_passes(4, p) for p in (1, 2, 4, 8)] == [58, 30, 18, 14]
+
+
+def _lib_worker(rank, world, port, out):
+    """One rank: this library's partition operator (part = rank) on cuda:0,
+    partial output to the host, summed over gloo. (Every rank uses the one
+    test GPU for its own independent kernels; the reduce is on the CPU, so no
+    rank's kernels wait on another's.)"""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import paper_2406_17981_b200 as T
+
+        levels = [8, 6, 16]
+        bg = T.BlockGenerator.dyadic(levels)
+        x = oracle.Oracle().random_vector([3] + levels, 9, 0.5)
+        op = T.Operator.split_ex(bg, precision=T.C128, part=rank, nparts=world)
+        y = torch.from_numpy(op.apply(x).view(np.float64).copy())
+        partition.reduce_partials(y, dst=0)
+        if rank == 0:
+            s = int(np.prod(levels))
+            ys = np.concatenate(oracle.Oracle().dyadic_apply(levels, [x[i * s:(i + 1) * s] for i in range(3)],
+                                                             mode="signs"))
+            got = y.numpy().view(np.complex128)
+            out.put(float(np.linalg.norm(got - ys) / np.linalg.norm(ys)))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_library_partials_reduce_over_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lib_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert q.get(timeout=5) <= 1e-12
