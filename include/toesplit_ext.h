@@ -83,6 +83,16 @@ void ts_split_options_default(ts_split_options* opt);
 ts_status ts_operator_create_split_ex(const ts_block_generator* g, const ts_split_options* opt,
                                       ts_operator** out);
 
+/* The full circulant-embedding operator (ref engine_embed.cpp:61-168, the
+ * method the paper improves on) for block generators, on this library's own
+ * FFT passes: opt->precision (c64 / c128), opt->storage (AUTO: the (n+1)^d
+ * mirror corner of each unique component's (2n)^d symbol when every component
+ * has a sign on every axis and skew padding is zero), opt->device, opt->s0;
+ * part / nparts are ignored. Applies like a split operator (ts_operator_apply,
+ * _apply_device, _apply_batch_device). */
+ts_status ts_operator_create_embed_ex(const ts_block_generator* g, const ts_split_options* opt,
+                                      ts_operator** out);
+
 /* y = T x on device memory: x, y hold m components of prod(levels) elements of
  * the operator's precision (float2 / double2), may not alias; stream is a
  * cudaStream_t (NULL = legacy default stream). Asynchronous: returns after

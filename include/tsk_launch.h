@@ -116,6 +116,24 @@ int tsk_convert(const void* src, int32_t src_prec, void* dst, int32_t dst_prec, 
  * pad/extract the leading corner of a (2n)^d tensor */
 int tsk_embed_corner(int32_t d, const int64_t* levels, int32_t prec, const void* src, void* dst,
                      int32_t extract, void* stream);
+/* m x m block symbol of the full-embedding engine: n_unique blocks of
+ * block_elems elements (full (2n)^d or (n+1)^d mirror corner), comp_map and
+ * per-unique-component skew masks as in tsk_spectra. */
+typedef struct tsk_block_symbol {
+    const void* data;
+    int64_t block_elems;
+    int32_t m;
+    int32_t n_unique;
+    int32_t corner;
+    int32_t reserved;
+    uint32_t skew_mask[TSK_MAX_UNIQUE];
+    int8_t comp_map[TSK_MAX_M * TSK_MAX_M];
+} tsk_block_symbol;
+/* work_c[(2n)^d] <- sum_c' S_{map(c,c')} work_c' for the m component tensors
+ * (cstride elements apart), per frequency; mirrored corner entries take the
+ * component's sign per mirrored skew axis (ref engine_embed.cpp:136-147). */
+int tsk_block_symbol_multiply(int32_t d, const int64_t* levels, int32_t prec, void* work, int64_t cstride,
+                              const tsk_block_symbol* sym, void* stream);
 /* work *= symbol, full (2n)^d symbol or (n+1)^d mirror corner with sign */
 int tsk_symbol_multiply(int32_t d, const int64_t* levels, int32_t prec, void* work,
                         const void* symbol, int32_t corner, int32_t skew, void* stream);

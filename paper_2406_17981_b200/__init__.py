@@ -46,11 +46,12 @@ EXTENSION_SYMBOLS = [
     "ts_device_count", "ts_operator_profile_device", "ts_generator_get_lags",
     "ts_device_memory_stats", "ts_device_memory_reset_peak", "ts_operator_create_split_multi",
     "ts_comm_unique_id", "ts_comm_create", "ts_comm_destroy", "ts_operator_apply_device_comm",
+    "ts_operator_create_embed_ex",
 ]
 LAUNCHER_SYMBOLS = [
     "tsk_fwd_split", "tsk_inv_merge", "tsk_leaf_pair", "tsk_embed_generator", "tsk_embed_dyadic",
     "tsk_fold_axis", "tsk_mirror_check", "tsk_store_block", "tsk_convert", "tsk_embed_corner",
-    "tsk_symbol_multiply", "tsk_embed_fold0",
+    "tsk_symbol_multiply", "tsk_embed_fold0", "tsk_block_symbol_multiply",
 ]
 
 
@@ -162,6 +163,7 @@ def _load():
     L.ts_device_count.restype = C.c_int32
     L.ts_operator_profile_device.argtypes = [_vp, _vp, _vp, _vp, C.POINTER(TsLaunchRecord),
                                              C.c_int32, C.POINTER(C.c_int32)]
+    L.ts_operator_create_embed_ex.argtypes = [_vp, C.POINTER(TsSplitOptions), C.POINTER(_vp)]
     L.ts_device_memory_stats.argtypes = [C.c_int32, C.POINTER(TsMemoryStats)]
     L.ts_device_memory_reset_peak.argtypes = [C.c_int32]
     L.ts_operator_create_split_multi.argtypes = [_vp, C.POINTER(TsSplitOptions), C.c_int32,
@@ -396,6 +398,18 @@ class Operator:
         opt.part, opt.nparts, opt.s0_re, opt.s0_im = part, nparts, s0.real, s0.imag
         h = _vp()
         _ok(lib.ts_operator_create_split_ex(bg._h, C.byref(opt), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def embed_ex(cls, bg: BlockGenerator, precision=C128, storage=STORAGE_AUTO, device=-1, s0=0j):
+        """Full circulant-embedding operator for block generators on this
+        library's FFT passes (ts_operator_create_embed_ex)."""
+        opt = TsSplitOptions()
+        lib.ts_split_options_default(C.byref(opt))
+        opt.precision, opt.storage, opt.device = precision, storage, device
+        opt.s0_re, opt.s0_im = s0.real, s0.imag
+        h = _vp()
+        _ok(lib.ts_operator_create_embed_ex(bg._h, C.byref(opt), C.byref(h)))
         return cls(h)
 
     @classmethod

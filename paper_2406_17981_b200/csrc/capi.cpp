@@ -363,6 +363,20 @@ ts_status ts_operator_create_split_ex(const ts_block_generator* g, const ts_spli
     });
 }
 
+ts_status ts_operator_create_embed_ex(const ts_block_generator* g, const ts_split_options* opt,
+                                      ts_operator** out)
+{
+    return guarded([&] {
+        need(g && out);
+        ts_split_options o;
+        ts_split_options_default(&o);
+        if (opt)
+            o = *opt;
+        auto dev = create_embed_block(g->g, o);
+        *out = new ts_operator{OperatorHandle{std::move(dev)}};
+    });
+}
+
 ts_status ts_operator_apply_device(const ts_operator* op, const void* x, void* y, void* stream,
                                    ts_metrics* metrics)
 {

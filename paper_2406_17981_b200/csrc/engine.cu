@@ -366,92 +366,147 @@ std::shared_ptr<DeviceOperator> create_split(const BlockGenerator& g, const ts_s
 
 // ---------------------------------------------------------------- embed
 
-std::shared_ptr<DeviceOperator> create_embed(const Generator& g, cplx s0, ts_storage storage)
+// Full circulant embedding (the method the paper improves on; ref
+// engine_embed.cpp:61-168) on this library's own FFT passes, for m x m block
+// generators in complex64 / complex128: per unique component the (2n)^d
+// symbol (or its (n+1)^d mirror corner) is computed on the device in
+// complex128 and stored in the operator precision.
+std::shared_ptr<DeviceOperator> create_embed_block(const BlockGenerator& g, const ts_split_options& opt)
 {
     const auto t0 = std::chrono::steady_clock::now();
-    if (storage != TS_STORAGE_AUTO && storage != TS_STORAGE_FULL && storage != TS_STORAGE_COMPRESSED)
+    if (opt.precision != TS_PREC_C128 && opt.precision != TS_PREC_C64)
+        fail(TS_ERR_INVALID_ARGUMENT, "invalid precision value");
+    if (opt.storage != TS_STORAGE_AUTO && opt.storage != TS_STORAGE_FULL &&
+        opt.storage != TS_STORAGE_COMPRESSED)
         fail(TS_ERR_INVALID_ARGUMENT, "invalid storage value");
-    bool compress = storage == TS_STORAGE_AUTO
-                        ? (g.symmetry == TS_SYM_SYMMETRIC || (g.symmetry == TS_SYM_SKEW && s0 == cplx{}))
-                        : storage == TS_STORAGE_COMPRESSED;
-    if (compress && g.symmetry == TS_SYM_GENERAL)
+    if (g.m > TSK_MAX_M || g.n_unique > TSK_MAX_UNIQUE)
+        fail(TS_ERR_SHAPE, "block arity too large for the embedding engine");
+    const cplx s0{opt.s0_re, opt.s0_im};
+    bool all_signed = true, any_skew = false;
+    for (int v : g.axis_sign) {
+        all_signed = all_signed && v != 0;
+        any_skew = any_skew || v < 0;
+    }
+    const bool compress = opt.storage == TS_STORAGE_AUTO ? all_signed && (!any_skew || s0 == cplx{})
+                                                         : opt.storage == TS_STORAGE_COMPRESSED;
+    if (compress && !all_signed)
         fail(TS_ERR_SYMMETRY, "compression requires a symmetric or skew generator");
-    DeviceGuard guard(-1);
+    DeviceGuard guard(opt.device);
     auto op = std::make_shared<DeviceOperator>();
     cuda_check(cudaGetDevice(&op->device), "cudaGetDevice");
+    const int d = static_cast<int>(g.levels.size());
     op->is_embed = true;
     op->levels = g.levels;
-    op->d = static_cast<int>(g.levels.size());
+    op->d = d;
     op->s = volume(g.levels);
-    op->prec = 0;
+    op->m = g.m;
+    op->n_unique = g.n_unique;
+    op->comp_map = g.comp_map;
+    op->axis_sign = g.axis_sign;
+    op->prec = opt.precision;
     op->embed_corner = compress;
-    op->embed_skew = g.symmetry == TS_SYM_SKEW;
-    Shape eshape(op->d);
-    for (int a = 0; a < op->d; ++a)
+    op->tskf_symmetry = g.scalar_symmetry >= 0 ? g.scalar_symmetry : 255;
+    for (int u = 0; u < g.n_unique; ++u) {
+        uint32_t mask = 0;
+        for (int a = 0; a < d; ++a)
+            if (g.axis_sign[u * d + a] < 0)
+                mask |= 1u << a;
+        op->skew_mask.push_back(mask);
+    }
+    Shape eshape(d);
+    for (int a = 0; a < d; ++a)
         eshape[a] = 2 * g.levels[a];
-    fill_tables(*op, eshape, op->tab2);
+    fill_tables(*op, eshape, op->tab2);  // operator precision, for the apply
+    std::vector<std::shared_ptr<AxisTables>> tabs64;  // complex128, for the symbol
+    {
+        DeviceOperator tmp;
+        tmp.prec = 0;
+        fill_tables(tmp, eshape, tabs64);
+    }
     const int64_t evol = volume(eshape);
+    int64_t blk = evol;
+    if (compress) {
+        blk = 1;
+        for (auto n : g.levels)
+            blk *= n + 1;
+    }
+    op->block_elems.assign(1, blk);
+    op->symbol = DevBuf(static_cast<size_t>(blk) * g.n_unique * op->es(), MEM_SPECTRA);
+    op->spectra_elems = static_cast<uint64_t>(blk) * g.n_unique;
     cudaStream_t st;
     cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
     struct StreamGuard {
         cudaStream_t s;
         ~StreamGuard() { cudaStreamDestroy(s); }
     } sg{st};
-    DevBuf spec(static_cast<size_t>(evol) * 16, MEM_SPECTRA);
-    {
-        DevBuf lags(g.lags.size() * 16, MEM_STAGING);
-        cuda_check(cudaMemcpyAsync(lags.p, g.lags.data(), g.lags.size() * 16,
-                                   cudaMemcpyHostToDevice, st),
-                   "upload");
-        launch_check(tsk_embed_generator(op->d, g.levels.data(), lags.p, s0.real(), s0.imag(),
-                                         spec.p, st),
-                     "embed");
-        for (int a = 0; a < op->d; ++a) {
-            tsk_axis x = axis_desc(eshape, op->tab2, a, 1, 0, 0);
+    DevBuf spec(static_cast<size_t>(evol) * 16, MEM_STAGING), lagbuf, chk(2 * sizeof(double), MEM_STAGING);
+    for (int u = 0; u < g.n_unique; ++u) {
+        if (g.dyadic) {
+            launch_check(tsk_embed_dyadic(d, g.levels.data(), g.dyadic_ij[u].first, g.dyadic_ij[u].second,
+                                          g.k, g.self_term.real(), g.self_term.imag(), s0.real(), s0.imag(),
+                                          spec.p, st),
+                         "embed dyadic");
+        } else {
+            const auto& lags = g.lags[u];
+            if (!lagbuf.p)
+                lagbuf = DevBuf(lags.size() * 16, MEM_STAGING);
+            cuda_check(cudaMemcpyAsync(lagbuf.p, lags.data(), lags.size() * 16, cudaMemcpyHostToDevice, st),
+                       "upload");
+            launch_check(tsk_embed_generator(d, g.levels.data(), lagbuf.p, s0.real(), s0.imag(), spec.p, st),
+                         "embed");
+        }
+        for (int a = 0; a < d; ++a) {
+            tsk_axis x = axis_desc(eshape, tabs64, a, 1, 0, 0);
             x.src0 = spec.p;
             x.dst0 = spec.p;
             x.use_odd = 0;
             launch_check(tsk_fwd_split(&x, st), "symbol fft");
         }
-        cuda_check(cudaStreamSynchronize(st), "sync");
+        char* dst = static_cast<char*>(op->symbol.p) + static_cast<size_t>(u) * blk * op->es();
+        if (compress) {
+            launch_check(tsk_mirror_check(d, eshape.data(), 0, op->skew_mask[u], spec.p,
+                                          static_cast<double*>(chk.p), st),
+                         "mirror check");
+            double h[2];
+            cuda_check(cudaMemcpyAsync(h, chk.p, sizeof h, cudaMemcpyDeviceToHost, st), "check");
+            cuda_check(cudaStreamSynchronize(st), "sync");
+            if (!(h[1] <= 1e-9 * std::max(h[0], 1.0)))
+                fail(TS_ERR_SYMMETRY, std::string("embedded spectrum is not mirror ") +
+                                          (op->skew_mask[u] ? "antisymmetric" : "symmetric"));
+            launch_check(tsk_store_block(d, eshape.data(), 0, 1, spec.p, dst, op->prec, st), "corner");
+        } else {
+            launch_check(tsk_convert(spec.p, 0, dst, op->prec, evol, st), "symbol");
+        }
     }
-    if (compress) {
-        DevBuf chk(2 * sizeof(double), MEM_STAGING);
-        const uint32_t mask = op->embed_skew ? ~0u : 0u;
-        launch_check(tsk_mirror_check(op->d, eshape.data(), 0, mask, spec.p,
-                                      static_cast<double*>(chk.p), st),
-                     "mirror check");
-        double h[2];
-        cuda_check(cudaMemcpyAsync(h, chk.p, sizeof h, cudaMemcpyDeviceToHost, st), "check");
-        cuda_check(cudaStreamSynchronize(st), "sync");
-        if (!(h[1] <= 1e-9 * std::max(h[0], 1.0)))
-            fail(TS_ERR_SYMMETRY, std::string("embedded spectrum is not mirror ") +
-                                      (op->embed_skew ? "antisymmetric" : "symmetric"));
-        int64_t corner = 1;
-        for (auto n : g.levels)
-            corner *= n + 1;
-        op->symbol = DevBuf(static_cast<size_t>(corner) * 16, MEM_SPECTRA);
-        launch_check(tsk_store_block(op->d, eshape.data(), 0, 1, spec.p, op->symbol.p, 0, st),
-                     "corner");
-        cuda_check(cudaStreamSynchronize(st), "sync");
-        op->spectra_elems = static_cast<uint64_t>(corner);
-    } else {
-        op->symbol = std::move(spec);
-        op->spectra_elems = static_cast<uint64_t>(evol);
-    }
+    cuda_check(cudaStreamSynchronize(st), "sync");
     op->precompute_ns = static_cast<uint64_t>(
         std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0)
             .count());
     return op;
 }
 
-// pad -> d forward passes -> symbol multiply -> d inverse passes -> project
-// (ref engine_embed.cpp:113-168)
+std::shared_ptr<DeviceOperator> create_embed(const Generator& g, cplx s0, ts_storage storage)
+{
+    ts_split_options o{};
+    o.precision = TS_PREC_C128;
+    o.storage = storage;
+    o.device = -1;
+    o.part = 0;
+    o.nparts = 1;
+    o.s0_re = s0.real();
+    o.s0_im = s0.imag();
+    return create_embed_block(block_from_scalar(g), o);
+}
+
+// pad -> d forward passes -> block symbol multiply -> d inverse passes ->
+// project, all m components per launch (ref engine_embed.cpp:113-168)
 void apply_embed(const DeviceOperator& op, const void* x, void* y, cudaStream_t st)
 {
     Shape eshape(op.d);
     for (int a = 0; a < op.d; ++a)
         eshape[a] = 2 * op.levels[a];
+    const int64_t evol = volume(eshape);
+    const size_t es = op.es();
     // stream-ordered scratch (metered; freed in stream order at scope exit)
     struct Scratch {
         void* p = nullptr;
@@ -469,27 +524,42 @@ void apply_embed(const DeviceOperator& op, const void* x, void* y, cudaStream_t 
             cudaFreeAsync(p, st);
             meter_sub(dev, MEM_WORK, n);
         }
-    } work(static_cast<size_t>(volume(eshape)) * op.es(), st);
-    launch_check(tsk_embed_corner(op.d, op.levels.data(), op.prec, x, work.p, 0, st), "pad");
+    } work(static_cast<size_t>(evol) * op.m * es, st);
+    char* wk = static_cast<char*>(work.p);
+    for (int c = 0; c < op.m; ++c)
+        launch_check(tsk_embed_corner(op.d, op.levels.data(), op.prec,
+                                      static_cast<const char*>(x) + c * op.s * es, wk + c * evol * es, 0, st),
+                     "pad");
     for (int a = 0; a < op.d; ++a) {
-        tsk_axis f = axis_desc(eshape, op.tab2, a, 1, 0, op.prec);
-        f.src0 = work.p;
-        f.dst0 = work.p;
+        tsk_axis f = axis_desc(eshape, op.tab2, a, op.m, evol, op.prec);
+        f.src0 = wk;
+        f.dst0 = wk;
         f.use_odd = 0;
         launch_check(tsk_fwd_split(&f, st), "embed fwd");
     }
-    launch_check(tsk_symbol_multiply(op.d, op.levels.data(), op.prec, work.p, op.symbol.p,
-                                     op.embed_corner ? 1 : 0, op.embed_skew ? 1 : 0, st),
-                 "symbol");
+    tsk_block_symbol bs{};
+    bs.data = op.symbol.p;
+    bs.block_elems = op.block_elems.empty() ? 0 : op.block_elems[0];
+    bs.m = op.m;
+    bs.n_unique = op.n_unique;
+    bs.corner = op.embed_corner ? 1 : 0;
+    for (int u = 0; u < op.n_unique; ++u)
+        bs.skew_mask[u] = op.skew_mask[u];
+    for (int i = 0; i < op.m * op.m; ++i)
+        bs.comp_map[i] = static_cast<int8_t>(op.comp_map[i]);
+    launch_check(tsk_block_symbol_multiply(op.d, op.levels.data(), op.prec, wk, evol, &bs, st), "symbol");
     for (int a = 0; a < op.d; ++a) {
-        tsk_axis iv = axis_desc(eshape, op.tab2, a, 1, 0, op.prec);
-        iv.src0 = work.p;
-        iv.dst0 = work.p;
+        tsk_axis iv = axis_desc(eshape, op.tab2, a, op.m, evol, op.prec);
+        iv.src0 = wk;
+        iv.dst0 = wk;
         iv.use_odd = 0;
         iv.scale = 1.0 / static_cast<double>(eshape[a]);
         launch_check(tsk_inv_merge(&iv, st), "embed inv");
     }
-    launch_check(tsk_embed_corner(op.d, op.levels.data(), op.prec, work.p, y, 1, st), "project");
+    for (int c = 0; c < op.m; ++c)
+        launch_check(tsk_embed_corner(op.d, op.levels.data(), op.prec, wk + c * evol * es,
+                                      static_cast<char*>(y) + c * op.s * es, 1, st),
+                     "project");
 }
 
 }  // namespace tsb

@@ -92,6 +92,7 @@ struct OperatorHandle {
 
 std::shared_ptr<DeviceOperator> create_split(const BlockGenerator& g, const ts_split_options& opt);
 std::shared_ptr<DeviceOperator> create_embed(const Generator& g, cplx s0, ts_storage storage);
+std::shared_ptr<DeviceOperator> create_embed_block(const BlockGenerator& g, const ts_split_options& opt);
 std::shared_ptr<DeviceOperator> load_split(const std::string& path);
 void save_kernel(const DeviceOperator& op, const std::string& path);
 void apply_host(const DeviceOperator& op, const double* v, double* y, const ts_policy* policy,

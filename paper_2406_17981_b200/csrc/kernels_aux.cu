@@ -341,6 +341,54 @@ __global__ void k_symbol_multiply(Shape32 lv, T2* __restrict__ work, const T2* _
     }
 }
 
+template <typename T2>
+__global__ void k_block_symbol(Shape32 lv, T2* __restrict__ work, int64_t cstride, tsk_block_symbol bs,
+                               int64_t total)
+{
+    const T2* sym = static_cast<const T2*>(bs.data);
+    GRID_STRIDE(off, total)
+    {
+        int64_t idx = off;
+        uint32_t mir = 0;  // axes read through the mirror
+        if (bs.corner) {
+            int64_t rem = off, cs = 1;
+            idx = 0;
+            for (int a = lv.d - 1; a >= 0; --a) {
+                const int64_t n = lv.n[a];
+                const int64_t l = rem % (2 * n);
+                rem /= 2 * n;
+                int64_t src = l;
+                if (l > n) {
+                    src = 2 * n - l;
+                    mir |= 1u << a;
+                }
+                idx += src * cs;
+                cs *= n + 1;
+            }
+        }
+        T2 xv[TSK_MAX_M];
+        for (int c = 0; c < bs.m; ++c)
+            xv[c] = work[c * cstride + off];
+        for (int c = 0; c < bs.m; ++c) {
+            T2 acc;
+            acc.x = 0;
+            acc.y = 0;
+            for (int c2 = 0; c2 < bs.m; ++c2) {
+                const int u = bs.comp_map[c * bs.m + c2];
+                T2 sv = sym[u * bs.block_elems + idx];
+                if (__popc(mir & bs.skew_mask[u]) & 1) {
+                    sv.x = -sv.x;
+                    sv.y = -sv.y;
+                }
+                const T2 p = cmul(sv, xv[c2]);
+                acc.x += p.x;
+                acc.y += p.y;
+            }
+            work[c * cstride + off] = acc;
+        }
+    }
+}
+
 }  // namespace tsk
 
 using namespace tsk;
@@ -420,6 +468,19 @@ int tsk_store_block(int32_t d, const int64_t* levels, uint32_t branch_bits, int3
     else
         k_store_block<double2><<<grid1d(total), 256, 0, (cudaStream_t)stream>>>(
             lv, branch_bits, compressed, (const double2*)block, (double2*)dst, total);
+    return (int)cudaGetLastError();
+}
+
+int tsk_block_symbol_multiply(int32_t d, const int64_t* levels, int32_t prec, void* work, int64_t cstride,
+                              const tsk_block_symbol* sym, void* stream)
+{
+    Shape32 lv = make_shape(d, levels);
+    const int64_t total = vol(lv) << d;
+    auto st = (cudaStream_t)stream;
+    if (prec)
+        tsk::k_block_symbol<float2><<<grid1d(total), 256, 0, st>>>(lv, (float2*)work, cstride, *sym, total);
+    else
+        tsk::k_block_symbol<double2><<<grid1d(total), 256, 0, st>>>(lv, (double2*)work, cstride, *sym, total);
     return (int)cudaGetLastError();
 }
 

@@ -370,6 +370,13 @@ static int dispatch_seg(const tsk_axis& a, cudaStream_t st)
     case 128: return launch<T, 128, MODE, SEG>(a, st);
     case 256: return launch<T, 256, MODE, SEG>(a, st);
     case 512: return launch<T, 512, MODE, SEG>(a, st);
+    // 1024 (the full-embedding engine's (2n)^d axes at n = 512): 128-byte
+    // rows (a 256-byte tile would need 256 KB of shared memory), complex64
+    case 1024:
+        if constexpr (sizeof(T) == 4)
+            return launch<T, 1024, MODE, 128>(a, st);
+        else
+            return -1;
     default: return -1;
     }
 }

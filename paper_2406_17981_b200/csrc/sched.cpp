@@ -528,12 +528,14 @@ void apply_batch_device(const DeviceOperator& op, const void* x, void* y, int64_
 
 void embed_counters(const DeviceOperator& op, ts_metrics* metrics)
 {
-    const uint64_t s = static_cast<uint64_t>(op.s);
-    metrics->fft_forward = static_cast<uint64_t>(op.d);
-    metrics->fft_inverse = static_cast<uint64_t>(op.d);
-    metrics->diag_mults = (uint64_t(1) << op.d) * s;
+    // ref engine_embed.cpp:113-168 per component; the m x m block multiply
+    // makes m^2 products per embedded frequency
+    const uint64_t s = static_cast<uint64_t>(op.s), mm = static_cast<uint64_t>(op.m);
+    metrics->fft_forward = static_cast<uint64_t>(op.d) * mm;
+    metrics->fft_inverse = static_cast<uint64_t>(op.d) * mm;
+    metrics->diag_mults = (uint64_t(1) << op.d) * s * mm * mm;
     metrics->phase_mults = 0;
-    metrics->peak_live_elems = static_cast<int64_t>(((uint64_t(1) << op.d) + 2) * s);
+    metrics->peak_live_elems = static_cast<int64_t>(((uint64_t(1) << op.d) + 2) * s * mm);
     metrics->kernel_elems = op.spectra_elems;
     metrics->precompute_ns = op.precompute_ns;
     metrics->apply_ns = 0;
@@ -562,8 +564,8 @@ void operator_info(const DeviceOperator& op, ts_operator_info* out)
             r.graph_replays += c->graph_replays;
     }
     if (op.is_embed) {
-        r.workspace_bytes = (static_cast<uint64_t>(1) << op.d) * op.s * op.es();
-        r.launches = 2 * op.d + 3;
+        r.workspace_bytes = (static_cast<uint64_t>(1) << op.d) * op.s * op.m * op.es();
+        r.launches = 2 * op.d + 1 + 2 * op.m;
     } else {
         r.workspace_bytes = work_bytes(op, 1);
         r.launches = count_launches(op.d, op.q);
