@@ -20,6 +20,7 @@ extern "C" int tsk_leaf1_pair(const tsk_axis* a, const tsk_spectra* sp, void* st
 extern "C" int tsk_global_fwd_split(const tsk_axis* a, void* stream);
 extern "C" int tsk_global_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_global_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
+extern "C" int tsk_contig_pass(const tsk_axis* a, int inv, void* stream);
 
 static bool env_flag(const char* name)
 {
@@ -56,6 +57,9 @@ extern "C" int tsk_fwd_split(const tsk_axis* a, void* stream)
         e = tsk_fast_fwd_split(a, stream);
         if (e != -1)
             return e;
+        e = tsk_contig_pass(a, 0, stream);
+        if (e != -1)
+            return e;
     }
     const int e = tsk_generic_fwd_split(a, stream);
     return e == -1 ? tsk_global_fwd_split(a, stream) : e;
@@ -68,6 +72,9 @@ extern "C" int tsk_inv_merge(const tsk_axis* a, void* stream)
         if (e != -1)
             return e;
         e = tsk_fast_inv_merge(a, stream);
+        if (e != -1)
+            return e;
+        e = tsk_contig_pass(a, 1, stream);
         if (e != -1)
             return e;
     }

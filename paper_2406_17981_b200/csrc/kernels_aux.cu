@@ -276,17 +276,17 @@ __global__ void k_c64_to_c128(const float2* __restrict__ s, double2* __restrict_
 
 // pad (extract == 0): dst[(2n)^d] = corner(src[n^d]) with zeros elsewhere;
 // extract: dst[n^d] = corner of src[(2n)^d]. One thread per big-tensor element.
-template <typename T2>
+template <typename T2, typename I = int64_t>
 __global__ void k_embed_corner(Shape32 lv, const T2* __restrict__ src, T2* __restrict__ dst,
                                int extract, int64_t total_big)
 {
     GRID_STRIDE(off, total_big)
     {
-        int64_t rem = off, small = 0, sstride = 1;
+        I rem = (I)off, small = 0, sstride = 1;  // I = 32-bit when the grid fits
         bool inside = true;
         for (int a = lv.d - 1; a >= 0; --a) {
-            const int64_t n = lv.n[a];
-            const int64_t j = rem % (2 * n);
+            const I n = (I)lv.n[a];
+            const I j = rem % (2 * n);
             rem /= 2 * n;
             if (j >= n)
                 inside = false;
@@ -341,7 +341,7 @@ __global__ void k_symbol_multiply(Shape32 lv, T2* __restrict__ work, const T2* _
     }
 }
 
-template <typename T2>
+template <typename T2, typename I>
 __global__ void k_block_symbol(Shape32 lv, T2* __restrict__ work, int64_t cstride, tsk_block_symbol bs,
                                int64_t total)
 {
@@ -351,20 +351,20 @@ __global__ void k_block_symbol(Shape32 lv, T2* __restrict__ work, int64_t cstrid
         int64_t idx = off;
         uint32_t mir = 0;  // axes read through the mirror
         if (bs.corner) {
-            int64_t rem = off, cs = 1;
-            idx = 0;
+            I rem = (I)off, cs = 1, acc = 0;  // I = 32-bit when the grid fits
             for (int a = lv.d - 1; a >= 0; --a) {
-                const int64_t n = lv.n[a];
-                const int64_t l = rem % (2 * n);
+                const I n = (I)lv.n[a];
+                const I l = rem % (2 * n);
                 rem /= 2 * n;
-                int64_t src = l;
+                I src = l;
                 if (l > n) {
                     src = 2 * n - l;
                     mir |= 1u << a;
                 }
-                idx += src * cs;
+                acc += src * cs;
                 cs *= n + 1;
             }
+            idx = (int64_t)acc;
         }
         T2 xv[TSK_MAX_M];
         for (int c = 0; c < bs.m; ++c)
@@ -477,10 +477,17 @@ int tsk_block_symbol_multiply(int32_t d, const int64_t* levels, int32_t prec, vo
     Shape32 lv = make_shape(d, levels);
     const int64_t total = vol(lv) << d;
     auto st = (cudaStream_t)stream;
-    if (prec)
-        tsk::k_block_symbol<float2><<<grid1d(total), 256, 0, st>>>(lv, (float2*)work, cstride, *sym, total);
+    const bool i32 = total < (int64_t(1) << 31);
+    if (prec && i32)
+        tsk::k_block_symbol<float2, int32_t><<<grid1d(total), 256, 0, st>>>(lv, (float2*)work, cstride, *sym, total);
+    else if (prec)
+        tsk::k_block_symbol<float2, int64_t><<<grid1d(total), 256, 0, st>>>(lv, (float2*)work, cstride, *sym, total);
+    else if (i32)
+        tsk::k_block_symbol<double2, int32_t><<<grid1d(total), 256, 0, st>>>(lv, (double2*)work, cstride, *sym,
+                                                                            total);
     else
-        tsk::k_block_symbol<double2><<<grid1d(total), 256, 0, st>>>(lv, (double2*)work, cstride, *sym, total);
+        tsk::k_block_symbol<double2, int64_t><<<grid1d(total), 256, 0, st>>>(lv, (double2*)work, cstride, *sym,
+                                                                            total);
     return (int)cudaGetLastError();
 }
 
@@ -506,9 +513,16 @@ int tsk_embed_corner(int32_t d, const int64_t* levels, int32_t prec, const void*
     for (int a = 0; a < d; ++a)
         total *= 2 * levels[a];
     auto st = (cudaStream_t)stream;
-    if (prec)
+    const bool i32 = total < (int64_t(1) << 31);
+    if (prec && i32)
+        k_embed_corner<float2, int32_t><<<grid1d(total), 256, 0, st>>>(lv, (const float2*)src, (float2*)dst,
+                                                                       extract, total);
+    else if (prec)
         k_embed_corner<float2><<<grid1d(total), 256, 0, st>>>(lv, (const float2*)src,
                                                               (float2*)dst, extract, total);
+    else if (i32)
+        k_embed_corner<double2, int32_t><<<grid1d(total), 256, 0, st>>>(lv, (const double2*)src, (double2*)dst,
+                                                                        extract, total);
     else
         k_embed_corner<double2><<<grid1d(total), 256, 0, st>>>(lv, (const double2*)src,
                                                                (double2*)dst, extract, total);

@@ -815,8 +815,98 @@ static int dispatch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
     return sp.compressed ? dispatch_s<T, M, true>(a, sp, st) : dispatch_s<T, M, false>(a, sp, st);
 }
 
+// ---- plain transforms along a contiguous axis (inner = 1, no split / no
+// merge partner): the full-embedding engine's last axis and the spectra
+// precompute. One fiber per TF = N/R threads (a warp or half warp), R
+// elements per thread, one shared-memory exchange (fft_one); out = F(x) or
+// scale * F^{-1}(x), natural order, in place allowed.
+template <typename T, int N, int R, bool INV>
+__global__ void __launch_bounds__(256) k_contig(tsk_axis p)
+{
+    using T2 = typename cx<T>::t;
+    constexpr int TF = N / R;
+    constexpr int P2 = N / R;
+    constexpr int FPC = 256 / TF;  // fibers per CTA
+    constexpr int NP = Pad<N, R>::NP;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T2* tw = reinterpret_cast<T2*>(smem_raw);
+    T2* bufs = tw + R * (P2 - 1);
+    for (int e = threadIdx.x; e < R * (P2 - 1); e += blockDim.x) {
+        const int j = e / (P2 - 1), r = e % (P2 - 1) + 1;
+        tw[e] = ldg_c(static_cast<const T2*>(p.roots) + (r * j) % N);
+    }
+    __syncthreads();
+    const int fi = threadIdx.x / TF, t = threadIdx.x % TF;
+    T2* buf = bufs + fi * NP;
+    const int64_t nfib = p.outer * p.ncomp;
+    const T scale = (T)p.scale;
+    const T2* src0 = static_cast<const T2*>(p.src0);
+    T2* dst0 = static_cast<T2*>(p.dst0);
+    // fibers are whole warps or half warps: the loop bound is uniform per
+    // fiber group, and fft_one synchronises with __syncwarp only
+    for (int64_t f0 = (int64_t)blockIdx.x * FPC; f0 < nfib; f0 += (int64_t)gridDim.x * FPC) {
+        const int64_t f = f0 + fi;
+        if (f >= nfib)
+            continue;
+        const int64_t c = f / p.outer, o = f - c * p.outer;
+        const int64_t off = c * p.cstride + o * N + t;
+        T2 v[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m)
+            v[m] = src0[off + m * TF];
+        fft_one<T, N, R, INV>(v, buf, tw, t);
+#pragma unroll
+        for (int m = 0; m < R; ++m)
+            dst0[off + m * TF] = INV ? scale_c<T>(v[m], scale) : v[m];
+    }
+}
+
+template <typename T, int N, int R, bool INV>
+static int launch_contig(const tsk_axis& a, cudaStream_t st)
+{
+    using T2 = typename cx<T>::t;
+    constexpr int TF = N / R;
+    constexpr int FPC = 256 / TF;
+    const size_t smem = sizeof(T2) * (R * (N / R - 1) + FPC * Pad<N, R>::NP);
+    auto kern = k_contig<T, N, R, INV>;
+    static thread_local int cached_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != cached_dev) {
+        if (int e = (int)cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
+            return e;
+        cached_dev = dev;
+    }
+    const int64_t nfib = a.outer * a.ncomp;
+    const int64_t blocks = (nfib + FPC - 1) / FPC;
+    const int64_t grid = blocks < sm_count() * 8 ? blocks : sm_count() * 8;
+    kern<<<(unsigned)(grid > 0 ? grid : 1), 256, smem, st>>>(a);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, bool INV>
+static int dispatch_contig(const tsk_axis& a, cudaStream_t st)
+{
+    switch (a.n) {
+    case 256: return launch_contig<T, 256, 16, INV>(a, st);
+    case 512: return launch_contig<T, 512, 32, INV>(a, st);
+    case 1024: return launch_contig<T, 1024, 32, INV>(a, st);
+    default: return -1;
+    }
+}
+
 }  // namespace leaf
 }  // namespace tsk
+
+// Plain (even-only) transform along a contiguous axis; -1: not covered.
+extern "C" int tsk_contig_pass(const tsk_axis* a, int inv, void* stream)
+{
+    if (a->inner != 1 || a->use_odd || !a->use_even || !a->prec || a->src1)
+        return -1;
+    auto st = (cudaStream_t)stream;
+    return inv ? tsk::leaf::dispatch_contig<float, true>(*a, st)
+               : tsk::leaf::dispatch_contig<float, false>(*a, st);
+}
 
 // -1: not covered (caller falls back), else the launch cudaError_t.
 extern "C" int tsk_leaf1_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream)

@@ -548,7 +548,7 @@ void operator_info(const DeviceOperator& op, ts_operator_info* out)
     r.m = op.m;
     r.n_unique = op.n_unique;
     r.precision = op.prec;
-    r.storage = op.compressed ? TS_STORAGE_COMPRESSED : TS_STORAGE_FULL;
+    r.storage = op.compressed || op.embed_corner ? TS_STORAGE_COMPRESSED : TS_STORAGE_FULL;
     r.is_embed = op.is_embed ? 1 : 0;
     r.device = op.device;
     r.part = op.part;
