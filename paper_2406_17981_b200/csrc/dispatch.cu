@@ -4,6 +4,7 @@
 // tile in shared memory) the global-memory long-axis passes.
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "tsk_launch.h"
@@ -48,38 +49,52 @@ static bool generic_only()
     return v;
 }
 
+// TSK_DEBUG_DISPATCH=1: print the kernel family each pass goes to (stderr)
+static bool debug_dispatch()
+{
+    static const bool v = env_flag("TSK_DEBUG_DISPATCH");
+    return v;
+}
+static int note(const char* pass, const char* fam, const tsk_axis* a, int e)
+{
+    if (debug_dispatch() && e != -1)
+        fprintf(stderr, "tsk %s: %s n=%lld inner=%lld outer=%lld ncomp=%d prec=%d -> %d\n", pass, fam,
+                (long long)a->n, (long long)a->inner, (long long)a->outer, a->ncomp, a->prec, e);
+    return e;
+}
+
 extern "C" int tsk_fwd_split(const tsk_axis* a, void* stream)
 {
     if (!generic_only()) {
-        int e = no_wide() ? -1 : tsk_wide_fwd_split(a, stream);
+        int e = no_wide() ? -1 : note("fwd", "wide", a, tsk_wide_fwd_split(a, stream));
         if (e != -1)
             return e;
-        e = tsk_fast_fwd_split(a, stream);
+        e = note("fwd", "fast", a, tsk_fast_fwd_split(a, stream));
         if (e != -1)
             return e;
-        e = tsk_contig_pass(a, 0, stream);
+        e = note("fwd", "contig", a, tsk_contig_pass(a, 0, stream));
         if (e != -1)
             return e;
     }
-    const int e = tsk_generic_fwd_split(a, stream);
-    return e == -1 ? tsk_global_fwd_split(a, stream) : e;
+    const int e = note("fwd", "generic", a, tsk_generic_fwd_split(a, stream));
+    return e == -1 ? note("fwd", "global", a, tsk_global_fwd_split(a, stream)) : e;
 }
 
 extern "C" int tsk_inv_merge(const tsk_axis* a, void* stream)
 {
     if (!generic_only()) {
-        int e = no_wide() ? -1 : tsk_wide_inv_merge(a, stream);
+        int e = no_wide() ? -1 : note("inv", "wide", a, tsk_wide_inv_merge(a, stream));
         if (e != -1)
             return e;
-        e = tsk_fast_inv_merge(a, stream);
+        e = note("inv", "fast", a, tsk_fast_inv_merge(a, stream));
         if (e != -1)
             return e;
-        e = tsk_contig_pass(a, 1, stream);
+        e = note("inv", "contig", a, tsk_contig_pass(a, 1, stream));
         if (e != -1)
             return e;
     }
-    const int e = tsk_generic_inv_merge(a, stream);
-    return e == -1 ? tsk_global_inv_merge(a, stream) : e;
+    const int e = note("inv", "generic", a, tsk_generic_inv_merge(a, stream));
+    return e == -1 ? note("inv", "global", a, tsk_global_inv_merge(a, stream)) : e;
 }
 
 static int leaf_one(const tsk_axis* a, const tsk_spectra* sp, void* stream)

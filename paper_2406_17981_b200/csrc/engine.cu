@@ -500,32 +500,14 @@ std::shared_ptr<DeviceOperator> create_embed(const Generator& g, cplx s0, ts_sto
 
 // pad -> d forward passes -> block symbol multiply -> d inverse passes ->
 // project, all m components per launch (ref engine_embed.cpp:113-168)
-void apply_embed(const DeviceOperator& op, const void* x, void* y, cudaStream_t st)
+void apply_embed(const DeviceOperator& op, const void* x, void* y, cudaStream_t st, void* work)
 {
     Shape eshape(op.d);
     for (int a = 0; a < op.d; ++a)
         eshape[a] = 2 * op.levels[a];
     const int64_t evol = volume(eshape);
     const size_t es = op.es();
-    // stream-ordered scratch (metered; freed in stream order at scope exit)
-    struct Scratch {
-        void* p = nullptr;
-        size_t n;
-        int dev = 0;
-        cudaStream_t st;
-        Scratch(size_t b, cudaStream_t s) : n(b), st(s)
-        {
-            cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-            cuda_check(cudaMallocAsync(&p, n, st), "cudaMallocAsync");
-            meter_add(dev, MEM_WORK, n);
-        }
-        ~Scratch()
-        {
-            cudaFreeAsync(p, st);
-            meter_sub(dev, MEM_WORK, n);
-        }
-    } work(static_cast<size_t>(evol) * op.m * es, st);
-    char* wk = static_cast<char*>(work.p);
+    char* wk = static_cast<char*>(work);
     for (int c = 0; c < op.m; ++c)
         launch_check(tsk_embed_corner(op.d, op.levels.data(), op.prec,
                                       static_cast<const char*>(x) + c * op.s * es, wk + c * evol * es, 0, st),

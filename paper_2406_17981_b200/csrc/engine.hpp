@@ -188,7 +188,8 @@ int64_t enqueue_apply(const DeviceOperator& op, ApplyCtx* ctx, const void* x, vo
 // component vector and hook(c) called after component c is enqueued.
 int64_t enqueue_apply_hooked(const DeviceOperator& op, ApplyCtx* ctx, const void* x, void* y,
                              int64_t nrhs, const std::function<void(int64_t)>& hook);
-void apply_embed(const DeviceOperator& op, const void* x, void* y, cudaStream_t st);
+// work: m (2n)^d elements of the operator precision (the apply context's)
+void apply_embed(const DeviceOperator& op, const void* x, void* y, cudaStream_t st, void* work);
 void embed_counters(const DeviceOperator& op, ts_metrics* m);
 void fill_counters(const DeviceOperator& op, ts_metrics* m, int64_t peak_vectors);
 uint64_t count_launches(int d, int q);

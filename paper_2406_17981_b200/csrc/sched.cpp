@@ -48,6 +48,8 @@ uint64_t DeviceOperator::cached_bytes() const
 
 static size_t work_bytes(const DeviceOperator& op, int64_t nrhs)
 {
+    if (op.is_embed)  // the (2n)^d padded copies of the m components
+        return static_cast<size_t>(op.s) * op.m * op.es() << op.d;
     const int nchild = std::max(0, op.d - 1 - op.q);
     return op.vec_bytes() * static_cast<size_t>(nrhs) * static_cast<size_t>(nchild);
 }
@@ -59,7 +61,7 @@ static constexpr size_t kMaxCtx = 8;
 
 ApplyCtx* acquire_ctx(const DeviceOperator& op, cudaStream_t stream, bool own, int64_t nrhs)
 {
-    const size_t need = op.is_embed ? 0 : work_bytes(op, nrhs);
+    const size_t need = op.multi || nrhs < 1 ? 0 : work_bytes(op, op.is_embed ? 1 : nrhs);
     std::unique_ptr<ApplyCtx> fresh;
     ApplyCtx* c = nullptr;
     {
@@ -503,9 +505,10 @@ void apply_batch_device(const DeviceOperator& op, const void* x, void* y, int64_
     DeviceGuard guard(op.device);
     int64_t peak = 2;
     if (op.is_embed) {
+        CtxLease lease(op, static_cast<cudaStream_t>(stream), false, 1);
         for (int64_t r = 0; r < nrhs; ++r)
             apply_embed(op, static_cast<const char*>(x) + op.vec_bytes() * r,
-                        static_cast<char*>(y) + op.vec_bytes() * r, static_cast<cudaStream_t>(stream));
+                        static_cast<char*>(y) + op.vec_bytes() * r, lease.c->st, lease.c->work.p);
     } else {
         CtxLease lease(op, static_cast<cudaStream_t>(stream), false, nrhs);
         peak = enqueue_apply(op, lease.c, x, y, nrhs);
@@ -564,7 +567,7 @@ void operator_info(const DeviceOperator& op, ts_operator_info* out)
             r.graph_replays += c->graph_replays;
     }
     if (op.is_embed) {
-        r.workspace_bytes = (static_cast<uint64_t>(1) << op.d) * op.s * op.m * op.es();
+        r.workspace_bytes = work_bytes(op, 1);
         r.launches = 2 * op.d + 1 + 2 * op.m;
     } else {
         r.workspace_bytes = work_bytes(op, 1);

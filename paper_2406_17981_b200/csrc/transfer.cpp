@@ -229,8 +229,7 @@ void apply_host(const DeviceOperator& op, const double* v, double* y, const ts_p
     // every policy runs the same device schedule here, so results are
     // bit-identical across policies as the reference requires)
     DeviceGuard guard(op.device);
-    const bool plain = !op.multi && !op.is_embed;
-    CtxLease lease(op, nullptr, true, plain ? 1 : 0);
+    CtxLease lease(op, nullptr, true, op.multi ? 0 : 1);
     ApplyCtx* c = lease.c;
     const size_t vb = op.vec_bytes();
     if (c->hx.bytes < vb) {
@@ -259,7 +258,7 @@ void apply_host(const DeviceOperator& op, const double* v, double* y, const ts_p
     if (op.multi)
         multi_apply_device(op, c->hx.p, c->hy.p, 1, c->st, nullptr);
     else if (op.is_embed)
-        apply_embed(op, c->hx.p, c->hy.p, c->st);
+        apply_embed(op, c->hx.p, c->hy.p, c->st, c->work.p);
     else
         peak = enqueue_apply(op, c, c->hx.p, c->hy.p, 1);
     cuda_check(cudaEventRecord(e1, c->st), "event");
