@@ -508,10 +508,30 @@ void apply_embed(const DeviceOperator& op, const void* x, void* y, cudaStream_t 
     const int64_t evol = volume(eshape);
     const size_t es = op.es();
     char* wk = static_cast<char*>(work);
-    for (int c = 0; c < op.m; ++c)
-        launch_check(tsk_embed_corner(op.d, op.levels.data(), op.prec,
-                                      static_cast<const char*>(x) + c * op.s * es, wk + c * evol * es, 0, st),
-                     "pad");
+    // d = 3: pad / project are a memset plus one pitched 3-D copy per component
+    // (copy-engine rates); other d: the index-mapping kernel
+    auto corner_copy = [&](const void* src, bool src_big, void* dst) {
+        const size_t rowb = static_cast<size_t>(op.levels[2]) * es;
+        cudaMemcpy3DParms p{};
+        const size_t bigp = 2 * rowb, smallp = rowb;
+        p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), src_big ? bigp : smallp, rowb,
+                                       static_cast<size_t>(src_big ? 2 * op.levels[1] : op.levels[1]));
+        p.dstPtr = make_cudaPitchedPtr(dst, src_big ? smallp : bigp, rowb,
+                                       static_cast<size_t>(src_big ? op.levels[1] : 2 * op.levels[1]));
+        p.extent = make_cudaExtent(rowb, static_cast<size_t>(op.levels[1]), static_cast<size_t>(op.levels[0]));
+        p.kind = cudaMemcpyDeviceToDevice;
+        cuda_check(cudaMemcpy3DAsync(&p, st), "corner copy");
+    };
+    for (int c = 0; c < op.m; ++c) {
+        const char* xc = static_cast<const char*>(x) + c * op.s * es;
+        char* wc = wk + c * evol * es;
+        if (op.d == 3) {
+            cuda_check(cudaMemsetAsync(wc, 0, static_cast<size_t>(evol) * es, st), "pad zero");
+            corner_copy(xc, false, wc);
+        } else {
+            launch_check(tsk_embed_corner(op.d, op.levels.data(), op.prec, xc, wc, 0, st), "pad");
+        }
+    }
     for (int a = 0; a < op.d; ++a) {
         tsk_axis f = axis_desc(eshape, op.tab2, a, op.m, evol, op.prec);
         f.src0 = wk;
@@ -538,10 +558,14 @@ void apply_embed(const DeviceOperator& op, const void* x, void* y, cudaStream_t 
         iv.scale = 1.0 / static_cast<double>(eshape[a]);
         launch_check(tsk_inv_merge(&iv, st), "embed inv");
     }
-    for (int c = 0; c < op.m; ++c)
-        launch_check(tsk_embed_corner(op.d, op.levels.data(), op.prec, wk + c * evol * es,
-                                      static_cast<char*>(y) + c * op.s * es, 1, st),
-                     "project");
+    for (int c = 0; c < op.m; ++c) {
+        char* yc = static_cast<char*>(y) + c * op.s * es;
+        if (op.d == 3)
+            corner_copy(wk + c * evol * es, true, yc);
+        else
+            launch_check(tsk_embed_corner(op.d, op.levels.data(), op.prec, wk + c * evol * es, yc, 1, st),
+                         "project");
+    }
 }
 
 }  // namespace tsb

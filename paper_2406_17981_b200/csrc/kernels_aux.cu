@@ -389,6 +389,60 @@ __global__ void k_block_symbol(Shape32 lv, T2* __restrict__ work, int64_t cstrid
     }
 }
 
+
+// As k_block_symbol, one row of the last axis per block iteration.
+__global__ void k_block_symbol_rows(Shape32 lv, float2* __restrict__ work, int64_t cstride, tsk_block_symbol bs,
+                                    int64_t rows)
+{
+    const float2* sym = static_cast<const float2*>(bs.data);
+    const int d = lv.d;
+    const int64_t nl = lv.n[d - 1], L = 2 * nl;
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+        // outer axes: row-uniform corner offset and mirror mask
+        int64_t rem = row, srow = 0, cs = 1;
+        uint32_t mir_row = 0;
+        for (int a = d - 2; a >= 0; --a) {
+            const int64_t n = lv.n[a];
+            const int64_t l = rem % (2 * n);
+            rem /= 2 * n;
+            int64_t src = l;
+            if (l > n) {
+                src = 2 * n - l;
+                mir_row |= 1u << a;
+            }
+            srow += src * cs;
+            cs *= n + 1;
+        }
+        for (int64_t j = threadIdx.x; j < L; j += blockDim.x) {
+            const int64_t off = row * L + j;
+            int64_t idx = off;
+            uint32_t mir = 0;
+            if (bs.corner) {
+                const int64_t jj = j > nl ? L - j : j;
+                idx = srow * (nl + 1) + jj;
+                mir = mir_row | (j > nl ? 1u << (d - 1) : 0u);
+            }
+            float2 xv[TSK_MAX_M];
+            for (int c = 0; c < bs.m; ++c)
+                xv[c] = work[c * cstride + off];
+            for (int c = 0; c < bs.m; ++c) {
+                float2 acc = make_float2(0.f, 0.f);
+                for (int c2 = 0; c2 < bs.m; ++c2) {
+                    const int u = bs.comp_map[c * bs.m + c2];
+                    float2 sv = sym[u * bs.block_elems + idx];
+                    if (__popc(mir & bs.skew_mask[u]) & 1) {
+                        sv.x = -sv.x;
+                        sv.y = -sv.y;
+                    }
+                    const float2 p = cmul(sv, xv[c2]);
+                    acc.x += p.x;
+                    acc.y += p.y;
+                }
+                work[c * cstride + off] = acc;
+            }
+        }
+    }
+}
 }  // namespace tsk
 
 using namespace tsk;
@@ -475,6 +529,16 @@ int tsk_block_symbol_multiply(int32_t d, const int64_t* levels, int32_t prec, vo
                               const tsk_block_symbol* sym, void* stream)
 {
     Shape32 lv = make_shape(d, levels);
+    if (prec && d >= 2 && 2 * levels[d - 1] <= 4096) {
+        // row-wise: the outer-axis mirror bookkeeping once per row (block),
+        // the last axis across the threads (coalesced reads of x and symbol)
+        int64_t rows = 1;
+        for (int a = 0; a < d - 1; ++a)
+            rows *= 2 * levels[a];
+        const unsigned grid = (unsigned)std::min<int64_t>(rows, 148 * 64);
+        tsk::k_block_symbol_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(lv, (float2*)work, cstride, *sym, rows);
+        return (int)cudaGetLastError();
+    }
     const int64_t total = vol(lv) << d;
     auto st = (cudaStream_t)stream;
     const bool i32 = total < (int64_t(1) << 31);
