@@ -269,7 +269,7 @@ constexpr int leaf1_g()
     return 128 / gcd_i(128, 4 * M * (N / R));
 }
 
-template <typename T, int N, int R, int M, bool CMP, int G = leaf1_g<N, R, M>()>
+template <typename T, int N, int R, int M, bool CMP, bool MRHS, int G = leaf1_g<N, R, M>()>
 // 16 elements per thread fit two 384-thread CTAs per SM (80 registers, 24
 // warps): the 256-point leaf 0.41 -> 0.365 ms at 256^3
 #ifndef TSK_LEAF256_2CTA
@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     // compressed: one unit = one mirror orbit; full storage: 4 consecutive
     // fibers; times nrhs right-hand sides, the RHS index fastest so that the
     // units sharing a spectra row run side by side (one HBM fetch per row)
-    const int64_t nrhs = p.nrhs > 1 ? p.nrhs : 1;
+    // (MRHS: a separate instantiation, so the single-vector pass keeps its
+    // register budget)
+    const int64_t nrhs = MRHS && p.nrhs > 1 ? p.nrhs : 1;
     const FastDiv divr((uint32_t)nrhs);
     const int64_t units = (CMP ? rest * st1 * st2 : (p.outer + 3) / 4) * nrhs;
     const T2* src0 = static_cast<const T2*>(p.src0);
@@ -423,7 +425,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
             u = units - 1;  // runs in lockstep (barriers), stores nothing
         const T2* src = src0;
         T2* dst = dst0;
-        if (nrhs > 1) {  // units < 2^31 (checked by the launcher)
+        if (MRHS && nrhs > 1) {  // units < 2^31 (checked by the launcher)
             const uint32_t ur = divr.div((uint32_t)u);
             const int64_t r = u - (int64_t)ur * nrhs;
             src += r * p.rstride;
@@ -736,7 +738,7 @@ static int sm_count()
     return sms > 0 ? sms : 148;
 }
 
-template <typename T, int N, int R, int M, bool CMP>
+template <typename T, int N, int R, int M, bool CMP, bool MRHS>
 static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
     using T2 = typename cx<T>::t;
@@ -748,7 +750,7 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         sizeof(T2) * (R * (N / R - 1) + G * 4 * M * NP + G * (M == 1 ? 1 : 6) * (N / 2 + 1));
     if (smem > 227 * 1024)
         return -1;
-    auto kern = k_leaf1<T, N, R, M, CMP>;
+    auto kern = k_leaf1<T, N, R, M, CMP, MRHS>;
     static thread_local int cached_dev = -1, cap = 0;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -796,17 +798,26 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
     return (int)cudaGetLastError();
 }
 
+template <typename T, int M, bool CMP, bool MRHS>
+static int dispatch_n(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
+{
+    switch (a.n) {
+    case 64: return launch<T, 64, 8, M, CMP, MRHS>(a, sp, st);
+    case 128: return launch<T, 128, 16, M, CMP, MRHS>(a, sp, st);
+    case 256: return launch<T, 256, 16, M, CMP, MRHS>(a, sp, st);
+    case 512:  // complex128 at R = 32 spills; the 8-point kernel handles it
+        if constexpr (sizeof(T) == 4)
+            return launch<T, 512, 32, M, CMP, MRHS>(a, sp, st);
+        else
+            return -1;
+    default: return -1;
+    }
+}
+
 template <typename T, int M, bool CMP>
 static int dispatch_s(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
-    switch (a.n) {
-    case 64: return launch<T, 64, 8, M, CMP>(a, sp, st);
-    case 128: return launch<T, 128, 16, M, CMP>(a, sp, st);
-    case 256: return launch<T, 256, 16, M, CMP>(a, sp, st);
-    case 512:  // complex128 at R = 32 spills; the 8-point kernel handles it
-        return sizeof(T) == 4 ? launch<T, 512, 32, M, CMP>(a, sp, st) : -1;
-    default: return -1;
-    }
+    return a.nrhs > 1 ? dispatch_n<T, M, CMP, true>(a, sp, st) : dispatch_n<T, M, CMP, false>(a, sp, st);
 }
 
 template <typename T, int M>
