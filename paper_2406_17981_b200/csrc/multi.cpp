@@ -23,6 +23,7 @@
 #include <nccl.h>  // types and prototypes only (resolved through dlsym)
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 namespace tsb {
@@ -48,9 +49,14 @@ const NcclApi& nccl()
     static const NcclApi api = [] {
         NcclApi a;
         void* h = nullptr;
-        for (const char* name : {"libnccl.so.2", "libnccl.so"})
-            if ((h = dlopen(name, RTLD_NOW | RTLD_GLOBAL)))
-                break;
+        // TSK_NCCL_LIB: another implementation of these entry points (the tests'
+        // single-process stand-in, tests/nccl_mock)
+        if (const char* alt = getenv("TSK_NCCL_LIB"); alt && *alt)
+            h = dlopen(alt, RTLD_NOW | RTLD_LOCAL);
+        else
+            for (const char* name : {"libnccl.so.2", "libnccl.so"})
+                if ((h = dlopen(name, RTLD_NOW | RTLD_GLOBAL)))
+                    break;
         if (!h) {
             const char* e = dlerror();
             a.why = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
@@ -171,7 +177,13 @@ std::shared_ptr<DeviceOperator> create_split_multi(const BlockGenerator& g, cons
     for (int i = 0; i < P; ++i) {
         if (devices[i] < 0 || devices[i] >= ndev)
             fail(TS_ERR_INVALID_ARGUMENT, "invalid device ordinal " + std::to_string(devices[i]));
-        for (int j = 0; j < i; ++j)
+        // (TSK_ALLOW_SHARED_DEVICE=1 lets tests place several parts on one
+        // GPU under the single-process NCCL stand-in; real NCCL refuses it)
+        static const bool shared_ok = [] {
+            const char* e = getenv("TSK_ALLOW_SHARED_DEVICE");
+            return e && e[0] == '1';
+        }();
+        for (int j = 0; j < i && !shared_ok; ++j)
             if (devices[j] == devices[i])
                 fail(TS_ERR_INVALID_ARGUMENT, "device ordinals must be distinct (one part per GPU)");
     }
