@@ -230,6 +230,9 @@ __device__ __forceinline__ void fft_one(typename cx<T>::t (&v)[R], typename cx<T
 #ifndef TSK_LEAF_MIXT
 #define TSK_LEAF_MIXT 1
 #endif
+#ifndef TSK_LEAF_XS
+#define TSK_LEAF_XS 1
+#endif
 // (Compressed storage only: with full storage the leaf reads each fiber's own
 // spectra from global memory and the extra registers of the TMEM chunks spill,
 // measured 3.83 -> 4.33 ms per launch at 512^3.)
@@ -291,6 +294,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     T2* bufs = tw + R * (P2 - 1);                      // G x CF x NP exchange / mix buffers
     T2* stg0 = bufs + G * CF * NP;                     // G x UM x LROW staged spectra rows
     __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t xbar[G];          // XS: x rows landed
 
     for (int e = threadIdx.x; e < R * (P2 - 1); e += NT) {
         const int j = e / (P2 - 1), r = e % (P2 - 1) + 1;
@@ -418,6 +422,105 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     const T2* spec = static_cast<const T2*>(sp.data);
     T2 ekeep[TM ? 1 : R];
 
+    // ---- unit geometry: fiber g of orbit member f, spectra row offsets,
+    // signs. Members past the orbit size alias a real member (loads stay in
+    // range) and skip the store.
+    auto geometry = [&](int64_t u, bool uvalid, bool& valid, int64_t& g, int64_t& off0, int64_t& off1,
+                        uint32_t& neg) {
+        neg = 0;
+        if constexpr (!CMP) {
+            g = u * 4 + f;
+            valid = uvalid && g < p.outer;
+            if (g >= p.outer)
+                g = p.outer - 1;
+            off0 = off1 = g * N;
+        } else {
+            // units < 2^31 (stored elements per component fit int32 here)
+            const uint32_t u32 = (uint32_t)u;
+            const uint32_t q2 = div2.div(u32), q1 = div1.div(q2);
+            const int s2 = (int)(u32 - q2 * (uint32_t)st2), s1 = (int)(q2 - q1 * (uint32_t)st1);
+            const int64_t r = q1;
+            int p1 = 0, p2 = 0;
+            const int c1 = A1 >= 0 ? orbit_members((int)n1, (bits >> A1) & 1u, s1, p1) : 1;
+            const int c2 = A2 >= 0 ? orbit_members((int)n2, (bits >> A2) & 1u, s2, p2) : 1;
+            valid = uvalid && f < c1 * c2;
+            const int i1 = c2 == 2 ? (f >> 1) & (c1 - 1) : f & (c1 - 1), i2 = f & (c2 - 1);
+            const int64_t kk1 = A1 < 0 ? 0 : (i1 ? p1 : s1);
+            const int64_t kk2 = A2 < 0 ? 0 : (i2 ? p2 : s2);
+            if (i1)
+                neg ^= mask1;
+            if (i2)
+                neg ^= mask2;
+            int64_t rsrc = 0, rstr = 1, gr = r, rfull = 0, rmul = 1;
+            for (int a = A1 - 1; a >= 0; --a) {
+                const int64_t na = sp.levels[a];
+                const int64_t ka = gr % na;
+                gr /= na;
+                const int odd = (bits >> a) & 1u;
+                bool mm;
+                rsrc += mirror_src(na, odd, ka, mm) * rstr;
+                rstr *= stored_len(na, odd);
+                rfull += ka * rmul;
+                rmul *= na;
+                if (mm)
+                    for (int uu = 0; uu < U; ++uu)
+                        neg ^= ((sp.skew_mask[uu] >> a) & 1u) << uu;
+            }
+            g = (rfull * n1 + kk1) * n2 + kk2;
+            const int64_t row = (rsrc * st1 + s1) * st2 + s2;
+            off0 = row * (N / 2 + 1);
+            off1 = row * (N / 2);
+        }
+    };
+    // XS (C3's 512-point 3x3 leaf): each unit's 12 x rows (4 fibers x 3
+    // components, 4 KB each) arrive in shared memory by bulk copies issued one
+    // unit ahead — while the current unit's odd branch computes — instead of
+    // per-thread global loads at the start of every unit (their latency was
+    // the largest stall); the odd branch re-reads x from the same rows.
+    constexpr bool XS = TSK_LEAF_XS && CMP && M == 3 && N == 512 && sizeof(T) == 4;
+    T2* xsu = stg0 + G * UM * LROW + (XS ? gi * CF * N : 0);  // this unit's rows
+    uint32_t xphase = 0;
+    auto issue_x = [&](int64_t tile_n) {
+        int64_t un = tile_n * G + gi;
+        if (un >= units)
+            un = units - 1;
+        const T2* srcn = src0;
+        if (MRHS && nrhs > 1) {
+            const uint32_t ur = divr.div((uint32_t)un);
+            srcn += (un - (int64_t)ur * nrhs) * p.rstride;
+            un = ur;
+        }
+        bool vn;
+        int64_t gn, o0, o1;
+        uint32_t ng;
+        geometry(un, true, vn, gn, o0, o1, ng);
+        if (t == 0 && c == 0) {
+            const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&xbar[gi]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(M * N * 8)
+                         : "memory");
+#pragma unroll
+            for (int cc = 0; cc < M; ++cc) {
+                const uint32_t dsts = (uint32_t)__cvta_generic_to_shared(xsu + (f * M + cc) * N);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        dsts),
+                    "l"(srcn + cc * p.cstride + gn * N), "r"(N * 8), "r"(bar)
+                    : "memory");
+            }
+        }
+    };
+    if constexpr (XS) {
+        if (threadIdx.x < G) {
+            const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&xbar[threadIdx.x]);
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(4) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncthreads();
+        if ((int64_t)blockIdx.x * G < units)
+            issue_x(blockIdx.x);
+    }
+
     for (int64_t tile = blockIdx.x; tile * G < units; tile += gridDim.x) {
         int64_t u = tile * G + gi;
         const bool uvalid = u < units;
@@ -432,56 +535,15 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
             dst += r * p.rstride;
             u = ur;
         }
-        // ---- unit geometry: fiber g of orbit member f, spectra row offsets,
-        // signs. Members past the orbit size alias a real member (loads stay in
-        // range) and skip the store.
-        auto geometry = [&](int64_t u, bool uvalid, bool& valid, int64_t& g, int64_t& off0, int64_t& off1,
-                            uint32_t& neg) {
-            neg = 0;
-            if constexpr (!CMP) {
-                g = u * 4 + f;
-                valid = uvalid && g < p.outer;
-                if (g >= p.outer)
-                    g = p.outer - 1;
-                off0 = off1 = g * N;
-            } else {
-                // units < 2^31 (stored elements per component fit int32 here)
-                const uint32_t u32 = (uint32_t)u;
-                const uint32_t q2 = div2.div(u32), q1 = div1.div(q2);
-                const int s2 = (int)(u32 - q2 * (uint32_t)st2), s1 = (int)(q2 - q1 * (uint32_t)st1);
-                const int64_t r = q1;
-                int p1 = 0, p2 = 0;
-                const int c1 = A1 >= 0 ? orbit_members((int)n1, (bits >> A1) & 1u, s1, p1) : 1;
-                const int c2 = A2 >= 0 ? orbit_members((int)n2, (bits >> A2) & 1u, s2, p2) : 1;
-                valid = uvalid && f < c1 * c2;
-                const int i1 = c2 == 2 ? (f >> 1) & (c1 - 1) : f & (c1 - 1), i2 = f & (c2 - 1);
-                const int64_t kk1 = A1 < 0 ? 0 : (i1 ? p1 : s1);
-                const int64_t kk2 = A2 < 0 ? 0 : (i2 ? p2 : s2);
-                if (i1)
-                    neg ^= mask1;
-                if (i2)
-                    neg ^= mask2;
-                int64_t rsrc = 0, rstr = 1, gr = r, rfull = 0, rmul = 1;
-                for (int a = A1 - 1; a >= 0; --a) {
-                    const int64_t na = sp.levels[a];
-                    const int64_t ka = gr % na;
-                    gr /= na;
-                    const int odd = (bits >> a) & 1u;
-                    bool mm;
-                    rsrc += mirror_src(na, odd, ka, mm) * rstr;
-                    rstr *= stored_len(na, odd);
-                    rfull += ka * rmul;
-                    rmul *= na;
-                    if (mm)
-                        for (int uu = 0; uu < U; ++uu)
-                            neg ^= ((sp.skew_mask[uu] >> a) & 1u) << uu;
-                }
-                g = (rfull * n1 + kk1) * n2 + kk2;
-                const int64_t row = (rsrc * st1 + s1) * st2 + s2;
-                off0 = row * (N / 2 + 1);
-                off1 = row * (N / 2);
-            }
-        };
+        if constexpr (XS) {  // this unit's x rows (issued one unit ahead)
+            const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&xbar[gi]);
+            asm volatile(
+                "{\n .reg .pred p;\n XW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra XW;\n}" ::"r"(
+                    bar),
+                "r"(xphase)
+                : "memory");
+            xphase ^= 1u;
+        }
         bool valid;
         int64_t g, off0, off1;
         uint32_t neg;
@@ -517,12 +579,19 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
         for (int beta = 0; beta < 2; ++beta) {
             if (beta == 0 ? !ue : !uo)
                 continue;
-            // x; the odd branch re-reads it (an L1 hit: the CTA's x rows fit next
-            // to its shared memory; measured faster than a TMEM copy)
+            // x: from the unit's shared-memory rows (XS), else global memory
+            // (the odd branch's re-read then hits L1)
             T2 v[R];
+            if constexpr (XS) {
+                const T2* xr = xsu + (f * M + c) * N + t;
 #pragma unroll
-            for (int m = 0; m < R; ++m)
-                v[m] = xin[m * TF];
+                for (int m = 0; m < R; ++m)
+                    v[m] = xr[m * TF];
+            } else {
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    v[m] = xin[m * TF];
+            }
             if (beta == 1) {
                 if constexpr (TWT) {
                     // P_k from this lane's TMEM table: one complex product
@@ -641,6 +710,10 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (beta == 0 && uo)
                 stage_row(1);
+            if constexpr (XS) {  // every thread of the unit has read its x rows
+                if ((beta == 1 || !uo) && (tile + gridDim.x) * G < units)
+                    issue_x(tile + gridDim.x);
+            }
             fft_one<T, N, R, true, TWT>(v, buf, tw, t, quad + TWOFF);
 
             if (beta == 0 && both) {
@@ -746,8 +819,9 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
     constexpr int NP = Pad<N, R>::NP;
     constexpr int G = leaf1_g<N, R, M>();
     constexpr int NT = G * 4 * M * TF;
-    const size_t smem =
-        sizeof(T2) * (R * (N / R - 1) + G * 4 * M * NP + G * (M == 1 ? 1 : 6) * (N / 2 + 1));
+    constexpr bool XS = TSK_LEAF_XS && CMP && M == 3 && N == 512 && sizeof(T) == 4;
+    const size_t smem = sizeof(T2) * (R * (N / R - 1) + G * 4 * M * NP + G * (M == 1 ? 1 : 6) * (N / 2 + 1) +
+                                      (XS ? G * 4 * M * N : 0));
     if (smem > 227 * 1024)
         return -1;
     auto kern = k_leaf1<T, N, R, M, CMP, MRHS>;
