@@ -14,6 +14,8 @@ extern "C" int tsk_generic_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_generic_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
 extern "C" int tsk_fast_fwd_split(const tsk_axis* a, void* stream);
 extern "C" int tsk_wide_fwd_split(const tsk_axis* a, void* stream);
+extern "C" int tsk_wtma_fwd_split(const tsk_axis* a, void* stream);
+extern "C" int tsk_wtma_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_wide_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_fast_inv_merge(const tsk_axis* a, void* stream);
 extern "C" int tsk_fast_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, void* stream);
@@ -66,7 +68,10 @@ static int note(const char* pass, const char* fam, const tsk_axis* a, int e)
 extern "C" int tsk_fwd_split(const tsk_axis* a, void* stream)
 {
     if (!generic_only()) {
-        int e = no_wide() ? -1 : note("fwd", "wide", a, tsk_wide_fwd_split(a, stream));
+        int e = no_wide() ? -1 : note("fwd", "wtma", a, tsk_wtma_fwd_split(a, stream));
+        if (e != -1)
+            return e;
+        e = no_wide() ? -1 : note("fwd", "wide", a, tsk_wide_fwd_split(a, stream));
         if (e != -1)
             return e;
         e = note("fwd", "fast", a, tsk_fast_fwd_split(a, stream));
@@ -83,7 +88,10 @@ extern "C" int tsk_fwd_split(const tsk_axis* a, void* stream)
 extern "C" int tsk_inv_merge(const tsk_axis* a, void* stream)
 {
     if (!generic_only()) {
-        int e = no_wide() ? -1 : note("inv", "wide", a, tsk_wide_inv_merge(a, stream));
+        int e = no_wide() ? -1 : note("inv", "wtma", a, tsk_wtma_inv_merge(a, stream));
+        if (e != -1)
+            return e;
+        e = no_wide() ? -1 : note("inv", "wide", a, tsk_wide_inv_merge(a, stream));
         if (e != -1)
             return e;
         e = note("inv", "fast", a, tsk_fast_inv_merge(a, stream));

@@ -1,0 +1,372 @@
+// Strided passes (K1 fwd_split, K3 inv_merge) at n = 512, complex64, with the
+// input tiles brought in by the Tensor Memory Accelerator.
+//
+// Why: a strided pass reads one 512-row x W-column tile per step. The DRAM
+// side wants wide row segments (256 B rows: 5.7-5.8 TB/s for the K1 pattern
+// against 4.4-5.2 at 128 B, tools/micro/strided_copy3.cu), but a 256 B tile
+// (128 KB) held by per-thread loads leaves room for one CTA per SM, whose
+// memory phase then idles while it computes (k_wide, kernels_wide.cu). Here
+// one CTA per SM keeps a single 128 KB landing buffer busy all the time: the
+// tile is copied from shared memory into registers (one 256 B row per warp
+// instruction, conflict free), and right after that copy the next tile's two
+// 256-row boxes are issued (cp.async.bulk.tensor, mbarrier completion) while
+// the current tile is transformed. The column FFT (R = 32 elements per
+// thread, radix 32 x 16) exchanges through a 64 KB half buffer in two rounds;
+// K1 parks x and K3 parks B(e) in tensor memory between their two
+// transforms; results go out as per-warp 256 B row stores.
+//
+// Same arithmetic, in the same order, as k_wide<float, 512, 32, W, MODE>
+// (bit-identical outputs); reference semantics as there (fft.cpp:65-87,
+// tensor.cpp:227-254, engine_split.cpp:13-37, relative to
+// /root/reference/proj/src/core).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "tsk_common.cuh"
+#include "tsk_tmem.cuh"
+#include "tsk_wide.cuh"
+
+namespace tsk {
+namespace wtma {
+
+using wide::cmul_tw;
+using wide::Dft;
+using wide::load_tw;
+using wide::Plan;
+using wide::Tw;
+
+constexpr int N = 512, R = 32, TF = N / R, W = 32, NT = TF * W;  // 512 threads
+constexpr int TILE_BYTES = N * W * 8;                            // 128 KB
+constexpr int BOX_ROWS = 256;
+using PL = Plan<N, R>;
+static_assert(PL::NST == 2 && PL::radix(0) == 32 && PL::radix(1) == 16, "radix 32 x 16");
+constexpr size_t SMEM = TILE_BYTES + (N / 2) * W * 8 + (PL::TW + N) * 8;
+
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// Radix-32 stage, exchange, radix-16 stage with twiddles: the arithmetic of
+// wide::fft_col<float, 512, 32, W, INV>. The exchange writes the stage-A
+// outputs (rows t*32 + q) and reads the row pattern (rows t + 16 m) through a
+// buffer of half the tile: round 0 moves q < 16 / even m (rows with r % 32 <
+// 16), round 1 q >= 16 / odd m.
+template <bool INV>
+__device__ __forceinline__ void fft_col(float2 (&v)[R], float2* xb, const float2* tw, int t, int w)
+{
+    Dft<float, R, INV>::run(v);
+    float2 ev[R / 2];
+#pragma unroll
+    for (int q = 0; q < R / 2; ++q)
+        xb[(t * 16 + q) * W + w] = v[q];
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < R / 2; ++h)
+        ev[h] = xb[(h * 16 + t) * W + w];  // m = 2h
+    __syncthreads();
+#pragma unroll
+    for (int q = R / 2; q < R; ++q)
+        xb[(t * 16 + q - 16) * W + w] = v[q];
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < R / 2; ++h) {
+        v[2 * h] = ev[h];
+        v[2 * h + 1] = xb[(h * 16 + t) * W + w];  // m = 2h + 1
+    }
+    __syncthreads();
+    // stage B: radix 16, Ns = 32, butterflies j = t + 16 i (i < 2)
+    constexpr int P = 16, G = 2;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const int jm = t + i * TF;
+#pragma unroll
+        for (int r = 1; r < P; ++r) {
+            const Tw<float> wv = load_tw<float>(tw + PL::tw_off(1) + jm * (P - 1) + (r - 1));
+            v[i + r * G] = cmul_tw<float, INV>(v[i + r * G], wv);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        float2 a[P];
+#pragma unroll
+        for (int r = 0; r < P; ++r)
+            a[r] = v[i + r * G];
+        Dft<float, P, INV>::run(a);
+#pragma unroll
+        for (int r = 0; r < P; ++r)
+            v[i + r * G] = a[r];
+    }
+}
+
+struct Maps {
+    CUtensorMap m[2];
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constant__ Maps maps)
+{
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    float2* land = reinterpret_cast<float2*>(smem_raw);     // N x W landing tile
+    float2* xb = land + N * W;                               // N/2 x W exchange half
+    float2* tw = xb + (N / 2) * W;                           // stage-B twiddles
+    float2* ph = tw + PL::TW;                                // split phase
+    __shared__ __align__(8) uint64_t full;
+    __shared__ uint32_t tmem_slot;
+
+    const float2* roots = static_cast<const float2*>(p.roots);
+    for (int e = threadIdx.x; e < PL::ns(1) * 15; e += NT) {
+        const int jm = e / 15, r = e % 15 + 1;
+        tw[PL::tw_off(1) + e] = ldg_c(roots + (r * jm) % N);
+    }
+    for (int k = threadIdx.x; k < N; k += NT)
+        ph[k] = ldg_c(static_cast<const float2*>(p.phase) + k);
+
+    const int w = threadIdx.x % W;
+    const int t = threadIdx.x / W;
+    const int64_t inner = p.inner;
+    const int64_t cols = inner / W;
+    const int64_t tpc = p.outer * cols;
+    const int64_t ntiles = tpc * p.ncomp;
+    const bool ue = p.use_even, uo = p.use_odd;
+    const float scale = (float)p.scale;
+    const int64_t rs = (int64_t)TF * inner;
+    // inputs per tile: K1 x; K3 B(e) and/or B(o)
+    const int nin = MODE == 0 ? 1 : (int)ue + (int)uo;
+    const int64_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t nloads = mine * nin;
+
+    // x (K1, both children) or B(e) (K3, both inputs) parked in tensor memory:
+    // 64 columns per thread, four warps per lane quadrant
+    const bool park = ue && uo;
+    uint32_t tbase = 0, lane_base = 0;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&full)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (park) {
+        tbase = tmem_alloc(&tmem_slot, 256);
+        const int warp = threadIdx.x / 32;
+        lane_base = tbase + ((uint32_t)(32 * (warp % 4)) << 16) + (uint32_t)(64 * (warp / 4));
+    } else {
+        __syncthreads();
+    }
+
+    const FastDiv div_tpc((uint32_t)tpc), div_cols((uint32_t)cols);
+    auto coords = [&](int64_t tile, int64_t& c, int64_t& o, int64_t& cb) {
+        const uint32_t t32 = (uint32_t)tile;
+        const uint32_t c32 = div_tpc.div(t32);
+        const uint32_t r32 = t32 - c32 * (uint32_t)tpc;
+        const uint32_t o32 = div_cols.div(r32);
+        c = c32;
+        o = o32;
+        cb = r32 - o32 * (uint32_t)cols;
+    };
+    // load g of this CTA: tile blockIdx.x + (g / nin) gridDim.x, input g % nin
+    auto issue = [&](int64_t g) {
+        const int64_t tile = blockIdx.x + (g / nin) * gridDim.x;
+        const int k = (int)(g % nin);
+        const int map = MODE == 0 ? 0 : (ue ? k : 1);
+        int64_t c, o, cb;
+        coords(tile, c, o, cb);
+        const int x = (int)(cb * W), z = (int)(c * p.outer + o);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full)),
+                     "r"(TILE_BYTES)
+                     : "memory");
+#pragma unroll
+        for (int r = 0; r < N; r += BOX_ROWS)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+                "[%2];" ::"r"(sa(land + r * W)),
+                "l"(&maps.m[map]), "r"(sa(&full)), "r"(x), "r"(r), "r"(z)
+                : "memory");
+    };
+    if (threadIdx.x == 0 && nloads > 0)
+        issue(0);
+    int64_t g = 0;
+    // take load g into registers, then hand the landing buffer to load g + 1
+    auto take = [&](float2(&v)[R]) {
+        asm volatile(
+            "{\n .reg .pred p;\n WT: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WT;\n}" ::"r"(
+                sa(&full)),
+            "r"((uint32_t)(g & 1))
+            : "memory");
+#pragma unroll
+        for (int m = 0; m < R; ++m)
+            v[m] = land[(t + m * TF) * W + w];
+        __syncthreads();
+        if (threadIdx.x == 0 && g + 1 < nloads)
+            issue(g + 1);
+        ++g;
+    };
+
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int64_t c, o, cb;
+        coords(tile, c, o, cb);
+        const int64_t base = c * p.cstride + o * (int64_t)N * inner + cb * W + w + (int64_t)t * inner;
+        float2 v[R];
+        if constexpr (MODE == 0) {
+            take(v);
+            if (uo) {
+                if (park)
+                    tmem_park<float, R, false>(lane_base, v);  // waited before the restore
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    v[m] = cmul_tw<float, false>(v[m], load_tw<float>(ph + t + m * TF));
+                fft_col<false>(v, xb, tw, t, w);
+                float2* dd = static_cast<float2*>(p.dst1) + base;
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    dd[m * rs] = v[m];
+                if (park) {
+                    tmem_wait_st();
+                    tmem_restore<float, R>(lane_base, v);
+                }
+            }
+            if (ue) {
+                fft_col<false>(v, xb, tw, t, w);
+                float2* de = static_cast<float2*>(p.dst0) + base;
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    de[m * rs] = v[m];
+            }
+        } else {
+            float2* dst = static_cast<float2*>(p.dst0) + base;
+            if (ue) {
+                take(v);
+                fft_col<true>(v, xb, tw, t, w);
+                if (!uo) {
+#pragma unroll
+                    for (int m = 0; m < R; ++m)
+                        dst[m * rs] = scale_c<float>(v[m], scale);
+                    continue;
+                }
+                tmem_park<float, R, false>(lane_base, v);  // waited before the restore
+            }
+            take(v);
+            fft_col<true>(v, xb, tw, t, w);
+#pragma unroll
+            for (int m = 0; m < R; ++m)
+                v[m] = cmul_tw<float, true>(v[m], load_tw<float>(ph + t + m * TF));
+            if (ue) {
+                // B(e) back 16 values at a time (the 128-register budget of
+                // 512 threads holds v and one chunk)
+                tmem_wait_st();
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t r32[32];
+                    tmem_ld32(lane_base + 32 * h, r32);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        v[16 * h + i] = cadd(v[16 * h + i], Words<float2>::make(r32 + 2 * i));
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < R; ++m)
+                dst[m * rs] = scale_c<float>(v[m], scale);
+        }
+    }
+    if (park)
+        tmem_free(tbase, 256);
+}
+
+// ---- host side ------------------------------------------------------------
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encoder()
+{
+    static const EncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<EncodeFn>(f);
+    }();
+    return fn;
+}
+
+// [outer * ncomp][N][inner] complex64 tensor as 8-byte elements; box W x 256 x 1
+static bool make_map(CUtensorMap* m, const void* base, const tsk_axis& a)
+{
+    EncodeFn enc = encoder();
+    if (!enc)
+        return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)a.inner, (cuuint64_t)N, (cuuint64_t)(a.outer * a.ncomp)};
+    const cuuint64_t strides[2] = {(cuuint64_t)a.inner * 8, (cuuint64_t)a.inner * N * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)W, (cuuint32_t)BOX_ROWS, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool disabled()
+{
+    static const bool v = [] {
+        const char* e = getenv("TSK_NO_WTMA");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+static int sm_count()
+{
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 148;
+}
+
+template <int MODE>
+static int launch(const tsk_axis& a, cudaStream_t st)
+{
+    if (disabled() || !a.prec || a.n != N || a.inner % W != 0 || a.cstride != a.outer * N * a.inner ||
+        !(a.use_even || a.use_odd))
+        return -1;
+    const int64_t ntiles = a.outer * (a.inner / W) * a.ncomp;
+    if (ntiles >= (int64_t(1) << 31) || a.outer * a.ncomp >= (int64_t(1) << 31) || a.inner >= (int64_t(1) << 31))
+        return -1;
+    const void* in0 = MODE == 0 ? a.src0 : (a.use_even ? a.src0 : a.src1);
+    if ((reinterpret_cast<uintptr_t>(in0) & 15) || (MODE == 1 && (reinterpret_cast<uintptr_t>(a.src1) & 15)))
+        return -1;
+    Maps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    if (!make_map(&maps.m[0], in0, a))
+        return -1;
+    if (MODE == 1 && a.use_even && a.use_odd && !make_map(&maps.m[1], a.src1, a))
+        return -1;
+    if (MODE == 1 && !a.use_even)
+        maps.m[1] = maps.m[0];
+    auto kern = k_wtma<MODE>;
+    static thread_local int cached_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != cached_dev) {
+        if (int e = (int)cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM))
+            return e;
+        cached_dev = dev;
+    }
+    const int64_t cap = sm_count();
+    const int64_t grid = ntiles < cap ? ntiles : cap;
+    kern<<<(unsigned)(grid > 0 ? grid : 1), NT, SMEM, st>>>(a, maps);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace wtma
+}  // namespace tsk
+
+// -1: shape not covered (the caller falls back), else the launch cudaError_t.
+extern "C" int tsk_wtma_fwd_split(const tsk_axis* a, void* stream)
+{
+    return tsk::wtma::launch<0>(*a, (cudaStream_t)stream);
+}
+
+extern "C" int tsk_wtma_inv_merge(const tsk_axis* a, void* stream)
+{
+    return tsk::wtma::launch<1>(*a, (cudaStream_t)stream);
+}

@@ -380,6 +380,39 @@ def test_wide_strided_passes_vs_oracle(levels):
         assert rel_l2(y64, y_or) <= 1e-5
 
 
+def test_tma_strided_passes_bit_identical_to_wide():
+    # complex64 n = 512 strided axes with 256-byte-multiple rows run the
+    # TMA-landing kernel (kernels_wtma.cu); TSK_NO_WTMA=1 (fresh process) runs
+    # k_wide instead: the same arithmetic in the same order, so bit-identical.
+    # Axis-0 and axis-1 passes, non-power-of-two column-block counts, in-place
+    # K1 below the root, the TMEM-parked K3, scalar and 3x3.
+    cases = [([512, 8, 32], T.SYM_GENERAL, T.C64, False), ([3, 512, 96], T.SYM_SYMMETRIC, T.C64, False),
+             ([512, 16, 32], 0, T.C64, True), ([2, 512, 160], T.SYM_SKEW, T.C64, False)]
+    wide = _run_with_env("TSK_NO_WTMA", cases)
+    for (levels, sym, prec, dyadic), yw in zip(cases, wide):
+        if dyadic:
+            x = O.random_vector([3] + levels, 19, 0.5)
+            op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec)
+        else:
+            g = T.Generator.random(levels, 13, 1.0, sym)
+            x = T.random_vector(levels, 13, 1.0)
+            op = T.Operator.split_ex(T.BlockGenerator.from_scalar(g), precision=prec)
+        assert np.array_equal(op.apply(x), yw), levels
+
+
+@pytest.mark.parametrize("nparts", [2, 4])
+def test_tma_strided_partitions_dyadic(nparts):
+    # single-child K1'/K3' (use_even or use_odd only) on a TMA-landing axis
+    levels = [512, 16, 32]
+    xs = _dyadic_x(levels, 23)
+    ys = np.concatenate(O.dyadic_apply(levels, xs, mode="signs"))
+    bg = T.BlockGenerator.dyadic(levels)
+    acc = np.zeros_like(ys)
+    for part in range(nparts):
+        acc += T.Operator.split_ex(bg, precision=T.C64, part=part, nparts=nparts).apply(np.concatenate(xs))
+    assert rel_l2(acc, ys) <= 1e-5
+
+
 @pytest.mark.parametrize("levels", [[512, 16, 16], [16, 256, 32]])
 def test_wide_dyadic_vs_oracle(levels):
     xs = _dyadic_x(levels, 7)
