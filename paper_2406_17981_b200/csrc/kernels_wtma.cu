@@ -1,5 +1,5 @@
-// Strided passes (K1 fwd_split, K3 inv_merge) at n = 512, complex64, with the
-// input tiles brought in by the Tensor Memory Accelerator.
+// Strided passes (K1 fwd_split, K3 inv_merge) at n = 512 and 256, complex64,
+// with the input tiles brought in by the Tensor Memory Accelerator.
 //
 // Why: a strided pass reads one 512-row x W-column tile per step. The DRAM
 // side wants wide row segments (256 B rows: 5.7-5.8 TB/s for the K1 pattern
@@ -10,12 +10,13 @@
 // tile is copied from shared memory into registers (one 256 B row per warp
 // instruction, conflict free), and right after that copy the next tile's two
 // 256-row boxes are issued (cp.async.bulk.tensor, mbarrier completion) while
-// the current tile is transformed. The column FFT (R = 32 elements per
-// thread, radix 32 x 16) exchanges through a 64 KB half buffer in two rounds;
+// the current tile is transformed. The column FFT (R = n/16 elements per
+// thread, radix R x 16) exchanges through shared memory (at n = 512 a 64 KB
+// half buffer in two rounds);
 // K1 parks x and K3 parks B(e) in tensor memory between their two
 // transforms; results go out as per-warp 256 B row stores.
 //
-// Same arithmetic, in the same order, as k_wide<float, 512, 32, W, MODE>
+// Same arithmetic, in the same order, as k_wide<float, n, n/16, W, MODE>
 // (bit-identical outputs); reference semantics as there (fft.cpp:65-87,
 // tensor.cpp:227-254, engine_split.cpp:13-37, relative to
 // /root/reference/proj/src/core).
@@ -38,48 +39,70 @@ using wide::load_tw;
 using wide::Plan;
 using wide::Tw;
 
-constexpr int N = 512, R = 32, TF = N / R, W = 32, NT = TF * W;  // 512 threads
-constexpr int TILE_BYTES = N * W * 8;                            // 128 KB
-constexpr int BOX_ROWS = 256;
-using PL = Plan<N, R>;
-static_assert(PL::NST == 2 && PL::radix(0) == 32 && PL::radix(1) == 16, "radix 32 x 16");
-constexpr size_t SMEM = TILE_BYTES + (N / 2) * W * 8 + (PL::TW + N) * 8;
+// N = 512 (R = 32, radix 32 x 16) or 256 (R = 16, radix 16 x 16); TF = 16
+// threads per column, W = 32 columns (256 B rows), 512 threads
+constexpr int TF = 16, W = 32, NT = TF * W, BOX_ROWS = 256;
+template <int N>
+struct Geo {
+    static constexpr int R = N / TF;
+    static constexpr int TILE_BYTES = N * W * 8;  // 128 / 64 KB
+    // exchange buffer: half a tile at N = 512 (two rounds), a whole one below
+    static constexpr int XROWS = N == 512 ? N / 2 : N;
+    using PL = Plan<N, R>;
+    static_assert(PL::NST == 2 && PL::radix(1) == 16, "two stages, radix R x 16");
+    static constexpr size_t SMEM = TILE_BYTES + XROWS * W * 8 + (PL::TW + N) * 8;
+    static constexpr int PW = 2 * R;   // TMEM words parked per thread
+    static constexpr int TCOLS = 4 * PW;  // four warps per lane quadrant
+};
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// Radix-32 stage, exchange, radix-16 stage with twiddles: the arithmetic of
-// wide::fft_col<float, 512, 32, W, INV>. The exchange writes the stage-A
-// outputs (rows t*32 + q) and reads the row pattern (rows t + 16 m) through a
-// buffer of half the tile: round 0 moves q < 16 / even m (rows with r % 32 <
+// Radix-R stage, exchange, radix-16 stage with twiddles: the arithmetic of
+// wide::fft_col<float, N, R, W, INV>. The exchange writes the stage-A outputs
+// (rows t R + q) and reads the row pattern (rows t + 16 m); at N = 512 through
+// a buffer of half the tile: round 0 moves q < 16 / even m (rows with r % 32 <
 // 16), round 1 q >= 16 / odd m.
-template <bool INV>
-__device__ __forceinline__ void fft_col(float2 (&v)[R], float2* xb, const float2* tw, int t, int w)
+template <int N, bool INV>
+__device__ __forceinline__ void fft_col(float2 (&v)[Geo<N>::R], float2* xb, const float2* tw, int t, int w)
 {
+    constexpr int R = Geo<N>::R;
+    using PL = typename Geo<N>::PL;
     Dft<float, R, INV>::run(v);
-    float2 ev[R / 2];
+    if constexpr (N == 512) {
+        float2 ev[R / 2];
 #pragma unroll
-    for (int q = 0; q < R / 2; ++q)
-        xb[(t * 16 + q) * W + w] = v[q];
-    __syncthreads();
+        for (int q = 0; q < R / 2; ++q)
+            xb[(t * 16 + q) * W + w] = v[q];
+        __syncthreads();
 #pragma unroll
-    for (int h = 0; h < R / 2; ++h)
-        ev[h] = xb[(h * 16 + t) * W + w];  // m = 2h
-    __syncthreads();
+        for (int h = 0; h < R / 2; ++h)
+            ev[h] = xb[(h * 16 + t) * W + w];  // m = 2h
+        __syncthreads();
 #pragma unroll
-    for (int q = R / 2; q < R; ++q)
-        xb[(t * 16 + q - 16) * W + w] = v[q];
-    __syncthreads();
+        for (int q = R / 2; q < R; ++q)
+            xb[(t * 16 + q - 16) * W + w] = v[q];
+        __syncthreads();
 #pragma unroll
-    for (int h = 0; h < R / 2; ++h) {
-        v[2 * h] = ev[h];
-        v[2 * h + 1] = xb[(h * 16 + t) * W + w];  // m = 2h + 1
+        for (int h = 0; h < R / 2; ++h) {
+            v[2 * h] = ev[h];
+            v[2 * h + 1] = xb[(h * 16 + t) * W + w];  // m = 2h + 1
+        }
+    } else {
+        // rows t R + q out, rows t + 16 m in (whole tile)
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+            xb[(t * R + q) * W + w] = v[q];
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < R; ++m)
+            v[m] = xb[(t + m * TF) * W + w];
     }
     __syncthreads();
-    // stage B: radix 16, Ns = 32, butterflies j = t + 16 i (i < 2)
-    constexpr int P = 16, G = 2;
+    // stage B: radix 16, Ns = R, butterflies j = t + 16 i (i < R / 16)
+    constexpr int P = 16, G = R / P;
 #pragma unroll
     for (int i = 0; i < G; ++i) {
-        const int jm = t + i * TF;
+        const int jm = (t + i * TF) % PL::ns(1);
 #pragma unroll
         for (int r = 1; r < P; ++r) {
             const Tw<float> wv = load_tw<float>(tw + PL::tw_off(1) + jm * (P - 1) + (r - 1));
@@ -103,13 +126,15 @@ struct Maps {
     CUtensorMap m[2];
 };
 
-template <int MODE>
+template <int N, int MODE>
 __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constant__ Maps maps)
 {
+    constexpr int R = Geo<N>::R;
+    using PL = typename Geo<N>::PL;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float2* land = reinterpret_cast<float2*>(smem_raw);     // N x W landing tile
-    float2* xb = land + N * W;                               // N/2 x W exchange half
-    float2* tw = xb + (N / 2) * W;                           // stage-B twiddles
+    float2* xb = land + N * W;                               // exchange rows
+    float2* tw = xb + Geo<N>::XROWS * W;                     // stage-B twiddles
     float2* ph = tw + PL::TW;                                // split phase
     __shared__ __align__(8) uint64_t full;
     __shared__ uint32_t tmem_slot;
@@ -117,7 +142,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
     const float2* roots = static_cast<const float2*>(p.roots);
     for (int e = threadIdx.x; e < PL::ns(1) * 15; e += NT) {
         const int jm = e / 15, r = e % 15 + 1;
-        tw[PL::tw_off(1) + e] = ldg_c(roots + (r * jm) % N);
+        tw[PL::tw_off(1) + e] = ldg_c(roots + (r * jm * (N / (PL::ns(1) * 16))) % N);
     }
     for (int k = threadIdx.x; k < N; k += NT)
         ph[k] = ldg_c(static_cast<const float2*>(p.phase) + k);
@@ -137,7 +162,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
     const int64_t nloads = mine * nin;
 
     // x (K1, both children) or B(e) (K3, both inputs) parked in tensor memory:
-    // 64 columns per thread, four warps per lane quadrant
+    // 2R columns per thread, four warps per lane quadrant
     const bool park = ue && uo;
     uint32_t tbase = 0, lane_base = 0;
     if (threadIdx.x == 0) {
@@ -145,9 +170,9 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (park) {
-        tbase = tmem_alloc(&tmem_slot, 256);
+        tbase = tmem_alloc(&tmem_slot, Geo<N>::TCOLS);
         const int warp = threadIdx.x / 32;
-        lane_base = tbase + ((uint32_t)(32 * (warp % 4)) << 16) + (uint32_t)(64 * (warp / 4));
+        lane_base = tbase + ((uint32_t)(32 * (warp % 4)) << 16) + (uint32_t)(Geo<N>::PW * (warp / 4));
     } else {
         __syncthreads();
     }
@@ -172,7 +197,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
         const int x = (int)(cb * W), z = (int)(c * p.outer + o);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full)),
-                     "r"(TILE_BYTES)
+                     "r"(Geo<N>::TILE_BYTES)
                      : "memory");
 #pragma unroll
         for (int r = 0; r < N; r += BOX_ROWS)
@@ -214,7 +239,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
 #pragma unroll
                 for (int m = 0; m < R; ++m)
                     v[m] = cmul_tw<float, false>(v[m], load_tw<float>(ph + t + m * TF));
-                fft_col<false>(v, xb, tw, t, w);
+                fft_col<N, false>(v, xb, tw, t, w);
                 float2* dd = static_cast<float2*>(p.dst1) + base;
 #pragma unroll
                 for (int m = 0; m < R; ++m)
@@ -225,7 +250,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
                 }
             }
             if (ue) {
-                fft_col<false>(v, xb, tw, t, w);
+                fft_col<N, false>(v, xb, tw, t, w);
                 float2* de = static_cast<float2*>(p.dst0) + base;
 #pragma unroll
                 for (int m = 0; m < R; ++m)
@@ -235,7 +260,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
             float2* dst = static_cast<float2*>(p.dst0) + base;
             if (ue) {
                 take(v);
-                fft_col<true>(v, xb, tw, t, w);
+                fft_col<N, true>(v, xb, tw, t, w);
                 if (!uo) {
 #pragma unroll
                     for (int m = 0; m < R; ++m)
@@ -245,7 +270,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
                 tmem_park<float, R, false>(lane_base, v);  // waited before the restore
             }
             take(v);
-            fft_col<true>(v, xb, tw, t, w);
+            fft_col<N, true>(v, xb, tw, t, w);
 #pragma unroll
             for (int m = 0; m < R; ++m)
                 v[m] = cmul_tw<float, true>(v[m], load_tw<float>(ph + t + m * TF));
@@ -254,7 +279,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
                 // 512 threads holds v and one chunk)
                 tmem_wait_st();
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < R / 16; ++h) {
                     uint32_t r32[32];
                     tmem_ld32(lane_base + 32 * h, r32);
 #pragma unroll
@@ -268,7 +293,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
         }
     }
     if (park)
-        tmem_free(tbase, 256);
+        tmem_free(tbase, Geo<N>::TCOLS);
 }
 
 // ---- host side ------------------------------------------------------------
@@ -290,14 +315,14 @@ static EncodeFn encoder()
     return fn;
 }
 
-// [outer * ncomp][N][inner] complex64 tensor as 8-byte elements; box W x 256 x 1
+// [outer * ncomp][n][inner] complex64 tensor as 8-byte elements; box W x 256 x 1
 static bool make_map(CUtensorMap* m, const void* base, const tsk_axis& a)
 {
     EncodeFn enc = encoder();
     if (!enc)
         return false;
-    const cuuint64_t dims[3] = {(cuuint64_t)a.inner, (cuuint64_t)N, (cuuint64_t)(a.outer * a.ncomp)};
-    const cuuint64_t strides[2] = {(cuuint64_t)a.inner * 8, (cuuint64_t)a.inner * N * 8};
+    const cuuint64_t dims[3] = {(cuuint64_t)a.inner, (cuuint64_t)a.n, (cuuint64_t)(a.outer * a.ncomp)};
+    const cuuint64_t strides[2] = {(cuuint64_t)a.inner * 8, (cuuint64_t)(a.inner * a.n * 8)};
     const cuuint32_t box[3] = {(cuuint32_t)W, (cuuint32_t)BOX_ROWS, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<void*>(base), dims, strides, box, es,
@@ -322,11 +347,10 @@ static int sm_count()
     return sms > 0 ? sms : 148;
 }
 
-template <int MODE>
+template <int N, int MODE>
 static int launch(const tsk_axis& a, cudaStream_t st)
 {
-    if (disabled() || !a.prec || a.n != N || a.inner % W != 0 || a.cstride != a.outer * N * a.inner ||
-        !(a.use_even || a.use_odd))
+    if (a.inner % W != 0 || a.cstride != a.outer * N * a.inner || !(a.use_even || a.use_odd))
         return -1;
     const int64_t ntiles = a.outer * (a.inner / W) * a.ncomp;
     if (ntiles >= (int64_t(1) << 31) || a.outer * a.ncomp >= (int64_t(1) << 31) || a.inner >= (int64_t(1) << 31))
@@ -342,7 +366,8 @@ static int launch(const tsk_axis& a, cudaStream_t st)
         return -1;
     if (MODE == 1 && !a.use_even)
         maps.m[1] = maps.m[0];
-    auto kern = k_wtma<MODE>;
+    auto kern = k_wtma<N, MODE>;
+    constexpr size_t SMEM = Geo<N>::SMEM;
     static thread_local int cached_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -357,16 +382,28 @@ static int launch(const tsk_axis& a, cudaStream_t st)
     return (int)cudaGetLastError();
 }
 
+template <int MODE>
+static int dispatch(const tsk_axis& a, cudaStream_t st)
+{
+    if (disabled() || !a.prec)
+        return -1;
+    switch (a.n) {
+    case 256: return launch<256, MODE>(a, st);
+    case 512: return launch<512, MODE>(a, st);
+    default: return -1;
+    }
+}
+
 }  // namespace wtma
 }  // namespace tsk
 
 // -1: shape not covered (the caller falls back), else the launch cudaError_t.
 extern "C" int tsk_wtma_fwd_split(const tsk_axis* a, void* stream)
 {
-    return tsk::wtma::launch<0>(*a, (cudaStream_t)stream);
+    return tsk::wtma::dispatch<0>(*a, (cudaStream_t)stream);
 }
 
 extern "C" int tsk_wtma_inv_merge(const tsk_axis* a, void* stream)
 {
-    return tsk::wtma::launch<1>(*a, (cudaStream_t)stream);
+    return tsk::wtma::dispatch<1>(*a, (cudaStream_t)stream);
 }
