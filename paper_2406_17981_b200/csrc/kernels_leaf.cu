@@ -132,6 +132,21 @@ __device__ __forceinline__ typename cx<T>::t cmac(typename cx<T>::t acc, typenam
     }
 }
 
+// acc (+)= -x * s
+template <typename T>
+__device__ __forceinline__ typename cx<T>::t cmac_neg(typename cx<T>::t acc, typename cx<T>::t x,
+                                                      typename cx<T>::t s, bool first)
+{
+    if constexpr (sizeof(T) == 4) {
+        const float2 nx = make_float2(-x.x, -x.y);
+        const float2 a = first ? mul2(nx, bc_x(s)) : fma2(nx, bc_x(s), acc);
+        return fma2(make_float2(x.y, -x.x), bc_y(s), a);
+    } else {
+        const typename cx<T>::t pr = cmul(x, s);
+        return first ? make_c<T>(-pr.x, -pr.y) : csub(acc, pr);
+    }
+}
+
 // a + e * scale
 template <typename T>
 __device__ __forceinline__ typename cx<T>::t fma_s(typename cx<T>::t e, T scale, typename cx<T>::t a)
@@ -272,7 +287,15 @@ constexpr int leaf1_g()
     return 128 / gcd_i(128, 4 * M * (N / R));
 }
 
-template <typename T, int N, int R, int M, bool CMP, bool MRHS, int G = leaf1_g<N, R, M>()>
+// FS (factorised signs; 3x3, d = 3, compressed, with the dyadic sign
+// structure skew_mask(i, j) = axis i XOR axis j): the mirror sign of block
+// (C, c') under the mirrored axis set F is s_C(F) s_c'(F), s_c(F) = -1 iff
+// axis c is in F. Component c's thread flips its transform by s_c once (c = 0,
+// 1: a per-fiber sign; c = 2: the leaf axis, known per element at compile
+// time), and y_C = s_C sum_c' T_Cc' (s_c' x_c'): the output sign folds into
+// the output scale (C = 0, 1) or into the partner terms (C = 2). No per-value
+// sign flips on the spectra reads.
+template <typename T, int N, int R, int M, bool CMP, bool MRHS, bool FS = false, int G = leaf1_g<N, R, M>()>
 // 16 elements per thread fit two 384-thread CTAs per SM (80 registers, 24
 // warps): the 256-point leaf 0.41 -> 0.365 ms at 256^3
 #ifndef TSK_LEAF256_2CTA
@@ -331,6 +354,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     // stage-B twiddles in TMEM (after the exchange blocks; 64 columns)
     constexpr bool TWT = leaf_twt<T, N, R, M, CMP, NW>();
     constexpr int TWOFF = 2 * MIXOFF;
+    static_assert(!FS || (TWT && M == 3 && CMP), "factorised signs: 3x3, compressed, TMEM twiddles");
     constexpr int PHOFF = TWOFF + 32 * (R / 16);  // phase table (TWT: 2R columns)
     uint32_t tbase = 0, lane_base = 0;
     if constexpr (TM) {
@@ -551,6 +575,11 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
         // sign masks per unique component: bit uu of neg (unmirrored k) and
         // of neg ^ lastneg (mirrored k)
         const uint32_t neg0 = neg, neg1 = neg ^ lastneg;
+        // FS: this thread's per-fiber sign s_c (c = 0: axis 0 mirrored, the
+        // sign of block (0, 2); c = 1: axis 1, block (1, 2)); the output scale
+        // carries it
+        const uint32_t sgx = FS && c < 2 ? (neg >> (c == 0 ? 2 : 4)) & 1u : 0u;
+        const T sscale = sgx ? -scale : scale;
         auto stage_row = [&](int beta) {
             if constexpr (!CMP)
                 return;
@@ -591,6 +620,12 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
 #pragma unroll
                 for (int m = 0; m < R; ++m)
                     v[m] = xin[m * TF];
+            }
+            if constexpr (FS) {
+                if (c < 2)
+#pragma unroll
+                    for (int m = 0; m < R; ++m)
+                        v[m] = flip_bits<T>(v[m], sgx);
             }
             if (beta == 1) {
                 if constexpr (TWT) {
@@ -674,7 +709,9 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                         else
                             ng = neg1;
                         T2 s_;
-                        if constexpr (CMP)
+                        if constexpr (FS)
+                            s_ = sp_[uu * LROW];
+                        else if constexpr (CMP)
                             s_ = flip_bits<T>(sp_[uu * LROW], (ng >> uu) & 1u);
                         else  // full storage: this fiber's own row, read once
                             s_ = ldg_c(spec + sp.branch_base[beta] + (beta ? off1 : off0) +
@@ -686,7 +723,18 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                             xv = xo[cc][m % XCH];
                         else
                             xv = fbufs[(f * M + cc) * NP + Pad<N, R>::rd(t, m)];
-                        acc = cmac<T>(acc, xv, s_, cc == 0);
+                        // FS: the term is negated on the mirrored leaf half iff
+                        // exactly one of C, cc is the leaf-axis component 2
+                        if constexpr (FS && ((C == 2) != (cc == 2))) {
+                            if (beta == 0 && 2 * m == R)  // k = N/2: unmirrored at t = 0
+                                acc = cmac<T>(acc, xv, flip_bits<T>(s_, t0 ? 0u : 1u), cc == 0);
+                            else if (mirm)
+                                acc = cmac_neg<T>(acc, xv, s_, cc == 0);
+                            else
+                                acc = cmac<T>(acc, xv, s_, cc == 0);
+                        } else {
+                            acc = cmac<T>(acc, xv, s_, cc == 0);
+                        }
                     });
                     v[m] = acc;
                     if (m % 2 == 1)
@@ -775,13 +823,13 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                                 a = wide::cmul_tw<T, true>(v[mi], w);
                                 if constexpr (bth)
                                     a = cadd(a, e[decltype(I)::value]);
-                                a = scale_c<T>(a, scale);
+                                a = scale_c<T>(a, FS ? sscale : scale);
                             } else if constexpr (odd) {
                                 a = PhaseR<T, R, true>::template apply<mi>(v[mi], pts);
                                 if constexpr (bth)
                                     a = fma_s<T>(e[decltype(I)::value], scale, a);
                             } else {
-                                a = scale_c<T>(v[mi], scale);
+                                a = scale_c<T>(v[mi], FS ? sscale : scale);
                             }
                             if (valid)
                                 yout[mi * TF] = a;
@@ -811,7 +859,7 @@ static int sm_count()
     return sms > 0 ? sms : 148;
 }
 
-template <typename T, int N, int R, int M, bool CMP, bool MRHS>
+template <typename T, int N, int R, int M, bool CMP, bool MRHS, bool FS = false>
 static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
     using T2 = typename cx<T>::t;
@@ -824,7 +872,7 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
                                       (XS ? G * 4 * M * N : 0));
     if (smem > 227 * 1024)
         return -1;
-    auto kern = k_leaf1<T, N, R, M, CMP, MRHS>;
+    auto kern = k_leaf1<T, N, R, M, CMP, MRHS, FS>;
     static thread_local int cached_dev = -1, cap = 0;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -872,18 +920,47 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
     return (int)cudaGetLastError();
 }
 
+// The dyadic sign structure (FS above): d = 3 and skew_mask(i, j) = axis i
+// XOR axis j for the canonical 6-unique 3x3 map. TSK_LEAF_NO_FS=1 (A/B)
+// keeps the per-value sign flips.
+static bool dyadic_signs(const tsk_spectra& sp)
+{
+    static const bool off = [] {
+        const char* e = getenv("TSK_LEAF_NO_FS");
+        return e && e[0] == '1';
+    }();
+    static const uint32_t want[6] = {0u, 3u, 5u, 0u, 6u, 0u};
+    if (off || sp.d != 3 || sp.m != 3 || sp.n_unique != 6 || !sp.compressed)
+        return false;
+    for (int u = 0; u < 6; ++u)
+        if (sp.skew_mask[u] != want[u])
+            return false;
+    return true;
+}
+
 template <typename T, int M, bool CMP, bool MRHS>
 static int dispatch_n(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
+    constexpr bool FSOK = sizeof(T) == 4 && M == 3 && CMP;
+    const bool fs = FSOK && a.n == 256 && dyadic_signs(sp);
     switch (a.n) {
     case 64: return launch<T, 64, 8, M, CMP, MRHS>(a, sp, st);
     case 128: return launch<T, 128, 16, M, CMP, MRHS>(a, sp, st);
-    case 256: return launch<T, 256, 16, M, CMP, MRHS>(a, sp, st);
+    case 256:
+        if constexpr (FSOK)
+            if (fs)
+                return launch<T, 256, 16, M, CMP, MRHS, true>(a, sp, st);
+        return launch<T, 256, 16, M, CMP, MRHS>(a, sp, st);
     case 512:  // complex128 at R = 32 spills; the 8-point kernel handles it
-        if constexpr (sizeof(T) == 4)
+        // (factorised signs measured slower at R = 32: K2 2.77 -> 3.06 ms at
+        // 512^3 with 144 B of spills at the 168-register cap — dropping only
+        // the diagonal blocks' flips spills as much; at R = 16, 80 registers,
+        // 0.367 -> 0.350 ms at 256^3; profiles/r02_ab_fs.txt)
+        if constexpr (sizeof(T) == 4) {
             return launch<T, 512, 32, M, CMP, MRHS>(a, sp, st);
-        else
+        } else {
             return -1;
+        }
     default: return -1;
     }
 }

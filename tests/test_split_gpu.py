@@ -466,6 +466,20 @@ def test_leaf_kernel_many_units_per_cta_vs_oracle():
     assert rel_l2(op.apply(np.concatenate(xs)), ys) <= 1e-5
 
 
+def test_leaf_factorised_signs_bit_identical():
+    # the dyadic 3x3 leaf with factorised mirror signs (component c flips its
+    # transform by s_c, the output sign rides on the scale) against the
+    # per-value spectra sign flips (TSK_LEAF_NO_FS=1, fresh process): every
+    # operation is sign-symmetric, so the results are bit-identical
+    cases = [([4, 3, 256], 0, T.C64, True), ([3, 2, 256], 0, T.C64, True), ([64, 48, 256], 0, T.C64, True),
+             ([1, 1, 256], 0, T.C64, True), ([4, 3, 512], 0, T.C64, True)]
+    ref = _run_with_env("TSK_LEAF_NO_FS", cases)
+    for (levels, _, prec, _), yr in zip(cases, ref):
+        x = O.random_vector([3] + levels, 19, 0.5)
+        op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=prec)
+        assert np.array_equal(op.apply(x), yr), levels
+
+
 @pytest.mark.parametrize("nparts", [2, 8])
 @pytest.mark.parametrize("n", [256, 512])
 def test_leaf_kernel_partitions(nparts, n):
