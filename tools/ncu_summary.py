@@ -1,14 +1,22 @@
 """Summarise an ncu report: per-kernel key metrics, SASS opcode mix and
-stall reasons (reads `ncu -i ... --page raw/source --csv`)."""
+stall reasons (reads `ncu -i ... --page raw/source --csv`).
+Usage: ncu_summary.py REP.ncu-rep [kernel-substring]
+       ncu_summary.py RAW.csv SASS.csv[.gz] [kernel-substring]  (exports made on the box)"""
 import collections
 import csv
 import io
 import subprocess
 import sys
 
+import gzip
+
 rep = sys.argv[1]
-kfilter = sys.argv[2] if len(sys.argv) > 2 else "k_"
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+pre = rep.endswith(".csv")
+kfilter = sys.argv[3 if pre else 2] if len(sys.argv) > (3 if pre else 2) else "k_"
+if pre:
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
 idx = {h: i for i, h in enumerate(hdr)}
@@ -28,9 +36,22 @@ for r in data:
     for w in want:
         if w in idx:
             print(f"  {w} = {r[idx[w]]} {units[idx[w]]}")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
-                      "regex:" + kfilter], capture_output=True, text=True).stdout
+if pre:
+    sp = sys.argv[2]
+    src = (gzip.open(sp, "rt") if sp.endswith(".gz") else open(sp)).read()
+else:
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
+                          "regex:" + kfilter], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
+if pre:  # keep only the sections of matching kernels
+    keep, cur = [], False
+    for r in rows:
+        if r and r[0] == "Kernel Name":
+            cur = kfilter in r[1]
+            continue
+        if cur:
+            keep.append(r)
+    rows = keep
 cnt = collections.Counter()
 stall = collections.Counter()
 tot = 0
