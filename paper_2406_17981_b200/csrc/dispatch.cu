@@ -37,6 +37,15 @@ static bool no_wide()
     return v;
 }
 
+// programmatic dependent launch of the hot passes (tsk_common.cuh)
+namespace tsk {
+bool pdl_enabled()
+{
+    static const bool v = !env_flag("TSK_NO_PDL");
+    return v;
+}
+}  // namespace tsk
+
 // TSK_NO_LEAF1=1 selects the 3-components-per-thread leaf kernel (A/B).
 static bool no_leaf1()
 {

@@ -534,6 +534,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
             }
         }
     };
+    pdl_wait();  // the previous pass's output is this pass's input
     if constexpr (XS) {
         if (threadIdx.x < G) {
             const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&xbar[threadIdx.x]);
@@ -546,6 +547,8 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     }
 
     for (int64_t tile = blockIdx.x; tile * G < units; tile += gridDim.x) {
+        if ((tile + gridDim.x) * G >= units)
+            pdl_trigger();  // last tile: the next pass may start its prologue
         int64_t u = tile * G + gi;
         const bool uvalid = u < units;
         if (!uvalid)
@@ -916,8 +919,8 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         return -1;
     const int64_t tiles = (units + G - 1) / G;
     const int64_t grid = tiles < cap ? tiles : cap;
-    kern<<<(unsigned)(grid > 0 ? grid : 1), NT, smem, st>>>(a, sp);
-    return (int)cudaGetLastError();
+    const cudaError_t e = launch_pdl(kern, (unsigned)(grid > 0 ? grid : 1), NT, smem, st, a, sp);
+    return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 
 // The dyadic sign structure (FS above): d = 3 and skew_mask(i, j) = axis i

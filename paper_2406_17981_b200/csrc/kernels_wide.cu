@@ -171,10 +171,13 @@ __global__ void __launch_bounds__(N / R * W, sizeof(T) == 4 && (N / R * W) < 512
         }
     }
 
+    pdl_wait();  // the previous pass's output is this pass's input
     // tile -> (component, outer, column block) by multiply-high (the
     // launcher guarantees ntiles < 2^31)
     const FastDiv div_tpc((uint32_t)tiles_per_comp), div_cols((uint32_t)cols);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (tile + gridDim.x >= ntiles)
+            pdl_trigger();  // last tile: the next pass may start its prologue
         const uint32_t t32 = (uint32_t)tile;
         const uint32_t c32 = div_tpc.div(t32);
         const uint32_t r32 = t32 - c32 * (uint32_t)tiles_per_comp;
@@ -341,8 +344,8 @@ static int launch(const tsk_axis& a, cudaStream_t st)
     if (ntiles >= (int64_t(1) << 31))
         return -1;  // 32-bit tile decomposition
     const int64_t grid = ntiles < cap ? ntiles : cap;
-    kern<<<(unsigned)(grid > 0 ? grid : 1), G::NT, smem, st>>>(a);
-    return (int)cudaGetLastError();
+    const cudaError_t e = launch_pdl(kern, (unsigned)(grid > 0 ? grid : 1), G::NT, smem, st, a);
+    return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 
 // Row segment per tile: 128 bytes, two CTAs per SM for K1 and K3 (with the

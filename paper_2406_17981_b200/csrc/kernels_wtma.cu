@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
                 "l"(&maps.m[map]), "r"(sa(&full)), "r"(x), "r"(r), "r"(z)
                 : "memory");
     };
+    pdl_wait();  // the previous pass's output is this pass's input
     if (threadIdx.x == 0 && nloads > 0)
         issue(0);
     int64_t g = 0;
@@ -227,6 +228,8 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
     };
 
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (tile + gridDim.x >= ntiles)
+            pdl_trigger();  // last tile: the next pass may start its prologue
         int64_t c, o, cb;
         coords(tile, c, o, cb);
         const int64_t base = c * p.cstride + o * (int64_t)N * inner + cb * W + w + (int64_t)t * inner;
@@ -378,8 +381,8 @@ static int launch(const tsk_axis& a, cudaStream_t st)
     }
     const int64_t cap = sm_count();
     const int64_t grid = ntiles < cap ? ntiles : cap;
-    kern<<<(unsigned)(grid > 0 ? grid : 1), NT, SMEM, st>>>(a, maps);
-    return (int)cudaGetLastError();
+    const cudaError_t e = launch_pdl(kern, (unsigned)(grid > 0 ? grid : 1), NT, SMEM, st, a, maps);
+    return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 
 template <int MODE>

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <utility>
 
 #include "tsk_launch.h"
 
@@ -333,6 +334,35 @@ struct FastDiv {
         return d > 1 ? __umulhi(n, mul) >> shift : n;
     }
 };
+
+// ---- programmatic dependent launch: the hot passes (k_wide, k_wtma,
+// k_leaf1) are launched with programmatic stream serialisation; each CTA of a
+// pass signals on its last tile, so the next pass's CTAs are scheduled as the
+// previous pass's CTAs retire and run their prologue (tables, tensor-memory
+// allocation, barriers) under its tail; each waits (griddepcontrol.wait: the
+// previous grid complete, its writes visible) before touching the vectors. A
+// no-op for plain launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // TSK_NO_PDL=1 turns it off (A/B); dispatch.cu
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                                     cudaStream_t st, Args&&... args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 #endif
 
 }  // namespace tsk
