@@ -259,6 +259,9 @@ constexpr bool leaf_mixt()
 #ifndef TSK_LEAF_TWT
 #define TSK_LEAF_TWT 1
 #endif
+#ifndef TSK_LEAF_FS512
+#define TSK_LEAF_FS512 1
+#endif
 // Stage-B twiddles (32 columns per radix-16 butterfly of a thread, R / 16 of
 // them) and the split phase (2R columns) in TMEM after the exchange blocks:
 // complex64, radix-16 stage B (N = 512 at R = 32, N = 256 at R = 16).
@@ -534,6 +537,12 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
             }
         }
     };
+    // N >= 256: one or two CTAs per SM holding most of the shared memory, so
+    // the next pass's CTAs cannot co-reside; they may be released at once.
+    // Smaller leaves release them on their last tile (a co-resident waiter
+    // would take issue slots from the pass).
+    if constexpr (N >= 256)
+        pdl_trigger();
     pdl_wait();  // the previous pass's output is this pass's input
     if constexpr (XS) {
         if (threadIdx.x < G) {
@@ -547,8 +556,10 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     }
 
     for (int64_t tile = blockIdx.x; tile * G < units; tile += gridDim.x) {
-        if ((tile + gridDim.x) * G >= units)
-            pdl_trigger();  // last tile: the next pass may start its prologue
+        if constexpr (N < 256) {
+            if ((tile + gridDim.x) * G >= units)
+                pdl_trigger();  // last tile: the next pass may start its prologue
+        }
         int64_t u = tile * G + gi;
         const bool uvalid = u < units;
         if (!uvalid)
@@ -674,18 +685,24 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                 const T2* sA = stg + t;
                 const T2* sB = stg + (N - beta - t);
                 const bool t0 = t == 0;
-                constexpr int XCH = 16 / Words<T2>::W;  // values per 16-column TMEM read
+                // 8-column reads at R = 32 (16 fewer live registers at the mix:
+                // the 168-register pass otherwise spills), 16 below
+                constexpr int WPC = R >= 32 ? 8 : 16;  // words per TMEM read
+                constexpr int XCH = WPC / Words<T2>::W;        // partner values per read
                 T2 xo[M][XCH];          // partners' values of the current chunk
 #pragma unroll
                 for (int m = 0; m < R; ++m) {
                     if constexpr (MIXT) {
                         if (m % XCH == 0) {
-                            constexpr int WPC = 16;  // words per chunk
-                            uint32_t r[M][16];
+                            uint32_t r[M][WPC];
 #pragma unroll
                             for (int cc = 0; cc < M; ++cc)
-                                if (cc != C)
-                                    tmem_ld16(quad + MIXOFF + EW * cc + (m / XCH) * WPC, r[cc]);
+                                if (cc != C) {
+                                    if constexpr (WPC == 8)
+                                        tmem_ld8(quad + MIXOFF + EW * cc + (m / XCH) * WPC, r[cc]);
+                                    else
+                                        tmem_ld16(quad + MIXOFF + EW * cc + (m / XCH) * WPC, r[cc]);
+                                }
                             tmem_wait_ld();
 #pragma unroll
                             for (int cc = 0; cc < M; ++cc)
@@ -925,7 +942,8 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 
 // The dyadic sign structure (FS above): d = 3 and skew_mask(i, j) = axis i
 // XOR axis j for the canonical 6-unique 3x3 map. TSK_LEAF_NO_FS=1 (A/B)
-// keeps the per-value sign flips.
+// keeps the per-value sign flips; TSK_LEAF_FS512=0 (build flag) keeps them at
+// n = 512.
 static bool dyadic_signs(const tsk_spectra& sp)
 {
     static const bool off = [] {
@@ -945,7 +963,7 @@ template <typename T, int M, bool CMP, bool MRHS>
 static int dispatch_n(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
 {
     constexpr bool FSOK = sizeof(T) == 4 && M == 3 && CMP;
-    const bool fs = FSOK && a.n == 256 && dyadic_signs(sp);
+    const bool fs = FSOK && (a.n == 256 || TSK_LEAF_FS512) && dyadic_signs(sp);
     switch (a.n) {
     case 64: return launch<T, 64, 8, M, CMP, MRHS>(a, sp, st);
     case 128: return launch<T, 128, 16, M, CMP, MRHS>(a, sp, st);
@@ -955,11 +973,17 @@ static int dispatch_n(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
                 return launch<T, 256, 16, M, CMP, MRHS, true>(a, sp, st);
         return launch<T, 256, 16, M, CMP, MRHS>(a, sp, st);
     case 512:  // complex128 at R = 32 spills; the 8-point kernel handles it
-        // (factorised signs measured slower at R = 32: K2 2.77 -> 3.06 ms at
-        // 512^3 with 144 B of spills at the 168-register cap — dropping only
-        // the diagonal blocks' flips spills as much; at R = 16, 80 registers,
-        // 0.367 -> 0.350 ms at 256^3; profiles/r02_ab_fs.txt)
+        // (factorised signs at R = 32 fit the 168-register cap only with the
+        // 8-column partner reads of the mix; with 16-column reads they spilled,
+        // K2 2.77 -> 3.06 ms at 512^3, profiles/r02_ab_fs.txt; with 8-column
+        // reads 2.81 -> 2.70 ms, profiles/r02_ab_fs512.txt. At R = 16, 80
+        // registers: 0.367 -> 0.350 ms at 256^3)
         if constexpr (sizeof(T) == 4) {
+#if TSK_LEAF_FS512
+            if constexpr (FSOK)
+                if (fs)
+                    return launch<T, 512, 32, M, CMP, MRHS, true>(a, sp, st);
+#endif
             return launch<T, 512, 32, M, CMP, MRHS>(a, sp, st);
         } else {
             return -1;

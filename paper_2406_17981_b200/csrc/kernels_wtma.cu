@@ -207,6 +207,10 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
                 "l"(&maps.m[map]), "r"(sa(&full)), "r"(x), "r"(r), "r"(z)
                 : "memory");
     };
+    // one CTA per SM with 130-200 KB of shared memory: the next pass's CTAs
+    // cannot co-reside, so they may be released at once (they are scheduled as
+    // these retire)
+    pdl_trigger();
     pdl_wait();  // the previous pass's output is this pass's input
     if (threadIdx.x == 0 && nloads > 0)
         issue(0);
@@ -228,8 +232,6 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
     };
 
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        if (tile + gridDim.x >= ntiles)
-            pdl_trigger();  // last tile: the next pass may start its prologue
         int64_t c, o, cb;
         coords(tile, c, o, cb);
         const int64_t base = c * p.cstride + o * (int64_t)N * inner + cb * W + w + (int64_t)t * inner;

@@ -19,6 +19,7 @@ CONFIGS = {
     "c0": ([16, 16, 16], "random", "c128", "full", 0, 1, 0),
     "c1": ([64, 64, 64], "dyadic", "c64", "full", None, 2, 1),
     "c1_128": ([64, 64, 64], "dyadic", "c128", "full", None, 2, 1),
+    "c1m": ([64, 64, 64], "dyadic", "c64", "auto", None, 2, 1),  # mirror-compressed spectra
     "c2": ([256, 256, 256], "dyadic", "c64", "auto", None, 3, 2),
     "c3": ([512, 512, 512], "dyadic", "c64", "auto", None, 4, 3),
     "c3full": ([512, 512, 512], "dyadic", "c64", "full", None, 4, 3),  # full 6-unique spectra

@@ -182,3 +182,30 @@ def test_split_engine_fails_loudly_without_gpu():
             make()
         assert e.value.code == T.TS_ERR_RESOURCE
         assert "GPU" in e.value.detail or "CUDA" in e.value.detail
+
+
+def test_hot_kernels_do_not_spill():
+    # the 512^3 passes sit at their register caps (k_leaf1: 168 at 384
+    # threads, k_wtma: 128 at 512); a spill there has cost 10% of the leaf pass
+    # (DESIGN.md), so the built library is checked for local memory use
+    import shutil
+    import subprocess
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "-res-usage", T.LIB_PATH], capture_output=True, text=True).stdout
+    # pattern: (instantiations, max stack bytes); the 256-point leaf runs two
+    # CTAs per SM at 80 registers with a 16-byte stack (measured: no cost)
+    hot = {r"k_leaf1IfLi512ELi32ELi3ELb1ELb0ELb[01]E": (2, 0), r"k_leaf1IfLi256ELi16ELi3ELb1ELb0ELb1E": (1, 16),
+           r"k_wtmaILi(512|256)ELi[01]E": (4, 0)}
+    lines = out.splitlines()
+    for pat, (want, stack) in hot.items():
+        found = 0
+        for i, ln in enumerate(lines):
+            if "Function" in ln and re.search(pat, ln):
+                found += 1
+                usage = lines[i + 1]
+                m = re.search(r"STACK:(\d+) ", usage)
+                assert m and int(m.group(1)) <= stack and "LOCAL:0 " in usage, (ln.strip(), usage.strip())
+        assert found == want, (pat, found)
