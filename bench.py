@@ -468,7 +468,7 @@ def e2e_comm(pop, x, y, xh, cdt, stream, args, rank, world, dev):
                    "subtrees, reduce) -> rank 0 -> pinned host y; serial, CUDA events, max over ranks"}
 
 
-SAMPLE_N = {"c0": 16, "c1": 64, "c1_128": 64, "c2": 128, "c3": 128, "c3full": 128, "c4": 32}
+SAMPLE_N = {"c0": 16, "c1": 64, "c1m": 64, "c1_128": 64, "c2": 128, "c3": 128, "c3full": 128, "c4": 32}
 CALIBRATION = os.path.join(ROOT, "profiles", "r02_reference_fullsize.json")
 
 

@@ -304,7 +304,13 @@ template <typename T, int N, int R, int M, bool CMP, bool MRHS, bool FS = false,
 #ifndef TSK_LEAF256_2CTA
 #define TSK_LEAF256_2CTA 1
 #endif
-__global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 * M * (N / R) < 384 ? 384 / (G * 4 * M * (N / R)) : (TSK_LEAF256_2CTA && sizeof(T) == 4 && R == 16 && N == 256 ? 2 : 1)) k_leaf1(tsk_axis p, tsk_spectra sp)
+// Short leaves (N = 64, complex64, 3x3: 384 threads) at two CTAs per SM as
+// well: their passes are a wave or two of tiles (configs[1]: 256 tiles), so a
+// second resident CTA per SM removes the second round
+#ifndef TSK_LEAF_SHORT_2CTA
+#define TSK_LEAF_SHORT_2CTA 1
+#endif
+__global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 * M * (N / R) < 384 ? 384 / (G * 4 * M * (N / R)) : (TSK_LEAF256_2CTA && sizeof(T) == 4 && R == 16 && N == 256 ? 2 : (TSK_LEAF_SHORT_2CTA && sizeof(T) == 4 && N <= 64 ? 2 : 1))) k_leaf1(tsk_axis p, tsk_spectra sp)
 {
     using T2 = typename cx<T>::t;
     constexpr int TF = N / R;
