@@ -57,6 +57,7 @@ def test_graph_replay_bit_identical_and_counted():
 
 @pytest.mark.parametrize("levels,prec,storage", [
     ([16, 16, 512], T.C64, T.STORAGE_AUTO),     # 512-point leaf, compressed
+    ([512, 16, 32], T.C64, T.STORAGE_AUTO),     # TMA strided passes over 3 x nrhs components
     ([8, 32, 256], T.C64, T.STORAGE_FULL),      # 256-point leaf, full storage
     ([4, 8, 64], T.C128, T.STORAGE_AUTO),       # complex128 leaf1
     ([5, 6, 7], T.C64, T.STORAGE_AUTO),         # generic kernels, per-RHS leaf launches

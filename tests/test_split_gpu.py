@@ -472,7 +472,8 @@ def test_leaf_factorised_signs_bit_identical():
     # per-value spectra sign flips (TSK_LEAF_NO_FS=1, fresh process): every
     # operation is sign-symmetric, so the results are bit-identical
     cases = [([4, 3, 256], 0, T.C64, True), ([3, 2, 256], 0, T.C64, True), ([64, 48, 256], 0, T.C64, True),
-             ([1, 1, 256], 0, T.C64, True), ([4, 3, 512], 0, T.C64, True)]
+             ([1, 1, 256], 0, T.C64, True), ([4, 3, 512], 0, T.C64, True), ([64, 48, 512], 0, T.C64, True),
+             ([1, 1, 512], 0, T.C64, True)]
     ref = _run_with_env("TSK_LEAF_NO_FS", cases)
     for (levels, _, prec, _), yr in zip(cases, ref):
         x = O.random_vector([3] + levels, 19, 0.5)
