@@ -514,6 +514,8 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     T2* xsu = stg0 + G * UM * LROW + (XS ? gi * CF * N : 0);  // this unit's rows
     uint32_t xphase = 0;
     auto issue_x = [&](int64_t tile_n) {
+        if (c != 0)  // warp-uniform: the component-0 warps issue for their fibers
+            return;
         int64_t un = tile_n * G + gi;
         if (un >= units)
             un = units - 1;
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
         int64_t gn, o0, o1;
         uint32_t ng;
         geometry(un, true, vn, gn, o0, o1, ng);
-        if (t == 0 && c == 0) {
+        if (t == 0) {
             const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&xbar[gi]);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(M * N * 8)
@@ -942,7 +944,7 @@ static int launch(const tsk_axis& a, const tsk_spectra& sp, cudaStream_t st)
         return -1;
     const int64_t tiles = (units + G - 1) / G;
     const int64_t grid = tiles < cap ? tiles : cap;
-    const cudaError_t e = launch_pdl(kern, (unsigned)(grid > 0 ? grid : 1), NT, smem, st, a, sp);
+    const cudaError_t e = launch_pdl(pdl_for(a), kern, (unsigned)(grid > 0 ? grid : 1), NT, smem, st, a, sp);
     return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 

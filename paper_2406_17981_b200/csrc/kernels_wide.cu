@@ -344,7 +344,7 @@ static int launch(const tsk_axis& a, cudaStream_t st)
     if (ntiles >= (int64_t(1) << 31))
         return -1;  // 32-bit tile decomposition
     const int64_t grid = ntiles < cap ? ntiles : cap;
-    const cudaError_t e = launch_pdl(kern, (unsigned)(grid > 0 ? grid : 1), G::NT, smem, st, a);
+    const cudaError_t e = launch_pdl(pdl_for(a), kern, (unsigned)(grid > 0 ? grid : 1), G::NT, smem, st, a);
     return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 

@@ -383,7 +383,7 @@ static int launch(const tsk_axis& a, cudaStream_t st)
     }
     const int64_t cap = sm_count();
     const int64_t grid = ntiles < cap ? ntiles : cap;
-    const cudaError_t e = launch_pdl(kern, (unsigned)(grid > 0 ? grid : 1), NT, SMEM, st, a, maps);
+    const cudaError_t e = launch_pdl(pdl_for(a), kern, (unsigned)(grid > 0 ? grid : 1), NT, SMEM, st, a, maps);
     return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 

@@ -347,8 +347,20 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 bool pdl_enabled();  // TSK_NO_PDL=1 turns it off (A/B); dispatch.cu
 
+// PDL pays where launch latency and pass prologues are a visible share
+// (configs[1] +11%, [4] +4%, [2] +1%); on 3.2 GB vectors it gained nothing
+// for compressed spectra and cost 16% with full 512^3 spectra (25.8 -> 30.0 ms
+// per MVM, profiles/r02_ab_ix.txt), so passes over vectors above 1 GB launch
+// plainly.
+__host__ inline bool pdl_for(const tsk_axis& a)
+{
+    const double bytes = (double)a.outer * (double)a.n * (double)a.inner * (double)(a.ncomp > 0 ? a.ncomp : 1) *
+                         (a.prec ? 8.0 : 16.0) * (double)(a.nrhs > 1 ? a.nrhs : 1);
+    return pdl_enabled() && bytes <= 1073741824.0;
+}
+
 template <typename... KArgs, typename... Args>
-static inline cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+static inline cudaError_t launch_pdl(bool use, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
                                      cudaStream_t st, Args&&... args)
 {
     cudaLaunchConfig_t cfg{};
@@ -358,7 +370,7 @@ static inline cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsi
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    at[0].val.programmaticStreamSerializationAllowed = use ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
