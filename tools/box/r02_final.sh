@@ -15,7 +15,7 @@ CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-embed-
 $CMD > gpurun_out/f_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/f_launches_bench_c3.csv $CMD > gpurun_out/f_ncu_launch.log 2>&1
 python tools/launch_times.py c3 1 > gpurun_out/f_plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_wtma<512, 1>" -s 2 -c 1 -o /tmp/f_k3 python tools/launch_times.py c3 1 > gpurun_out/f_ncu_k3.log 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_wtma<.int.512, .int.1>" -s 2 -c 1 -o /tmp/f_k3 python tools/launch_times.py c3 1 > gpurun_out/f_ncu_k3.log 2>&1
 ncu -i /tmp/f_k3.ncu-rep --page raw --csv > gpurun_out/f_k3_raw.csv 2>&1
 ncu -i /tmp/f_k3.ncu-rep --page source --csv --print-source sass > gpurun_out/f_k3_sass.csv 2>&1
 gzip -f gpurun_out/f_k3_sass.csv
