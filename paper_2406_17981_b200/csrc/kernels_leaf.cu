@@ -467,6 +467,22 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
             if (g >= p.outer)
                 g = p.outer - 1;
             off0 = off1 = g * N;
+        } else if constexpr (FS && N == 512) {
+            // d = 3 (FS): orbit axes 0 and 1, no rest axes (units = st1 st2)
+            // (at N = 256 the 80-register pass spills with this variant)
+            const uint32_t u32 = (uint32_t)u;
+            const uint32_t q2 = div2.div(u32);
+            const int s2 = (int)(u32 - q2 * (uint32_t)st2), s1 = (int)q2;
+            int p1 = 0, p2 = 0;
+            const int c1 = orbit_members((int)n1, bits & 1u, s1, p1);
+            const int c2 = orbit_members((int)n2, (bits >> 1) & 1u, s2, p2);
+            valid = uvalid && f < c1 * c2;
+            const int i1 = c2 == 2 ? (f >> 1) & (c1 - 1) : f & (c1 - 1), i2 = f & (c2 - 1);
+            neg = (i1 ? mask1 : 0u) ^ (i2 ? mask2 : 0u);
+            g = (int64_t)((i1 ? p1 : s1) * (int)n2 + (i2 ? p2 : s2));
+            const int row = s1 * (int)st2 + s2;
+            off0 = (int64_t)row * (N / 2 + 1);
+            off1 = (int64_t)row * (N / 2);
         } else {
             // units < 2^31 (stored elements per component fit int32 here)
             const uint32_t u32 = (uint32_t)u;
