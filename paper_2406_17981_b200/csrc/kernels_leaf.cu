@@ -147,6 +147,18 @@ __device__ __forceinline__ typename cx<T>::t cmac_neg(typename cx<T>::t acc, typ
     }
 }
 
+// e + o conj(w); packed f32x2: e rides on the first FFMA2 (w.x o + e, then
+// - w.y (i o)), one instruction fewer than a product and a sum
+template <typename T>
+__device__ __forceinline__ typename cx<T>::t cmulc_add(typename cx<T>::t o, typename cx<T>::t w,
+                                                       typename cx<T>::t e)
+{
+    if constexpr (sizeof(T) == 4)
+        return fma2(make_float2(o.y, -o.x), bc_y(w), fma2(o, bc_x(w), e));
+    else
+        return cadd(cmulc(o, w), e);
+}
+
 // a + e * scale
 template <typename T>
 __device__ __forceinline__ typename cx<T>::t fma_s(typename cx<T>::t e, T scale, typename cx<T>::t a)
@@ -247,6 +259,15 @@ __device__ __forceinline__ void fft_one(typename cx<T>::t (&v)[R], typename cx<T
 #endif
 #ifndef TSK_LEAF_XS
 #define TSK_LEAF_XS 1
+#endif
+// Streaming (st.global.cs, evict-first) output stores: K2 0.346 -> 0.341 ms at
+// 256^3, neutral at 512^3 (profiles/r02_ab_stcs.txt)
+#ifndef TSK_LEAF_STCS
+#define TSK_LEAF_STCS 1
+#endif
+// TSK_LEAF_LDEF=1 (A/B): the x-row bulk copies carry an L2 evict-first policy
+#ifndef TSK_LEAF_LDEF
+#define TSK_LEAF_LDEF 0
 #endif
 // (Compressed storage only: with full storage the leaf reads each fiber's own
 // spectra from global memory and the extra registers of the TMEM chunks spill,
@@ -550,14 +571,26 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(M * N * 8)
                          : "memory");
+#if TSK_LEAF_LDEF
+            uint64_t pol;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
 #pragma unroll
             for (int cc = 0; cc < M; ++cc) {
                 const uint32_t dsts = (uint32_t)__cvta_generic_to_shared(xsu + (f * M + cc) * N);
+#if TSK_LEAF_LDEF
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+                    "[%3], %4;" ::"r"(dsts),
+                    "l"(srcn + cc * p.cstride + gn * N), "r"(N * 8), "r"(bar), "l"(pol)
+                    : "memory");
+#else
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         dsts),
                     "l"(srcn + cc * p.cstride + gn * N), "r"(N * 8), "r"(bar)
                     : "memory");
+#endif
             }
         }
     };
@@ -864,9 +897,15 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                                 Tw<T> w;
                                 w.lo = ph[decltype(I)::value];
                                 w.hi = w.lo;
-                                a = wide::cmul_tw<T, true>(v[mi], w);
-                                if constexpr (bth)
-                                    a = cadd(a, e[decltype(I)::value]);
+                                // (fused at R = 32 only: the 80-register 256-point
+                                // pass spills 64 B with it)
+                                if constexpr (bth && R >= 32) {
+                                    a = cmulc_add<T>(v[mi], w.lo, e[decltype(I)::value]);
+                                } else {
+                                    a = wide::cmul_tw<T, true>(v[mi], w);
+                                    if constexpr (bth)
+                                        a = cadd(a, e[decltype(I)::value]);
+                                }
                                 a = scale_c<T>(a, FS ? sscale : scale);
                             } else if constexpr (odd) {
                                 a = PhaseR<T, R, true>::template apply<mi>(v[mi], pts);
@@ -875,8 +914,13 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
                             } else {
                                 a = scale_c<T>(v[mi], FS ? sscale : scale);
                             }
-                            if (valid)
-                                yout[mi * TF] = a;
+                            if (valid) {
+                                // (short leaves: their vectors are often L2-resident)
+                                if constexpr (TSK_LEAF_STCS && N >= 256)
+                                    __stcs(yout + mi * TF, a);
+                                else
+                                    yout[mi * TF] = a;
+                            }
                         });
                     });
                 };

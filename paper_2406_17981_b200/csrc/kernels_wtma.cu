@@ -126,6 +126,26 @@ struct Maps {
     CUtensorMap m[2];
 };
 
+// Output stores of the forward-split pass (one read, two writes) are marked
+// streaming (st.global.cs, evict-first): K1 1.70 -> 1.67 ms at 512^3; the merge
+// pass (two reads, one write) lost 1% with them and keeps plain stores
+// (profiles/r02_ab_stcs.txt). TSK_WTMA_STCS: bit 0 = K1, bit 1 = K3.
+#ifndef TSK_WTMA_STCS
+#define TSK_WTMA_STCS 1
+#endif
+// TSK_WTMA_LDEF=1 (A/B): the TMA tile loads carry an L2 evict-first policy
+#ifndef TSK_WTMA_LDEF
+#define TSK_WTMA_LDEF 0
+#endif
+template <int MODE>
+__device__ __forceinline__ void st_out(float2* p, float2 v)
+{
+    if constexpr (((TSK_WTMA_STCS) >> MODE) & 1)
+        __stcs(p, v);
+    else
+        *p = v;
+}
+
 template <int N, int MODE>
 __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constant__ Maps maps)
 {
@@ -199,6 +219,17 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full)),
                      "r"(Geo<N>::TILE_BYTES)
                      : "memory");
+#if TSK_WTMA_LDEF
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#pragma unroll
+        for (int r = 0; r < N; r += BOX_ROWS)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+                "{%3, %4, %5}], [%2], %6;" ::"r"(sa(land + r * W)),
+                "l"(&maps.m[map]), "r"(sa(&full)), "r"(x), "r"(r), "r"(z), "l"(pol)
+                : "memory");
+#else
 #pragma unroll
         for (int r = 0; r < N; r += BOX_ROWS)
             asm volatile(
@@ -206,6 +237,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
                 "[%2];" ::"r"(sa(land + r * W)),
                 "l"(&maps.m[map]), "r"(sa(&full)), "r"(x), "r"(r), "r"(z)
                 : "memory");
+#endif
     };
     // one CTA per SM with 130-200 KB of shared memory: the next pass's CTAs
     // cannot co-reside, so they may be released at once (they are scheduled as
@@ -248,7 +280,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
                 float2* dd = static_cast<float2*>(p.dst1) + base;
 #pragma unroll
                 for (int m = 0; m < R; ++m)
-                    dd[m * rs] = v[m];
+                    st_out<MODE>(dd + m * rs, v[m]);
                 if (park) {
                     tmem_wait_st();
                     tmem_restore<float, R>(lane_base, v);
@@ -259,7 +291,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
                 float2* de = static_cast<float2*>(p.dst0) + base;
 #pragma unroll
                 for (int m = 0; m < R; ++m)
-                    de[m * rs] = v[m];
+                    st_out<MODE>(de + m * rs, v[m]);
             }
         } else {
             float2* dst = static_cast<float2*>(p.dst0) + base;
@@ -269,7 +301,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
                 if (!uo) {
 #pragma unroll
                     for (int m = 0; m < R; ++m)
-                        dst[m * rs] = scale_c<float>(v[m], scale);
+                        st_out<MODE>(dst + m * rs, scale_c<float>(v[m], scale));
                     continue;
                 }
                 tmem_park<float, R, false>(lane_base, v);  // waited before the restore
@@ -294,7 +326,7 @@ __global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constan
             }
 #pragma unroll
             for (int m = 0; m < R; ++m)
-                dst[m * rs] = scale_c<float>(v[m], scale);
+                st_out<MODE>(dst + m * rs, scale_c<float>(v[m], scale));
         }
     }
     if (park)

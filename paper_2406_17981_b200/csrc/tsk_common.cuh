@@ -209,33 +209,55 @@ __device__ __forceinline__ void dft4<float, true>(float2& x0, float2& x1, float2
     x3 = add2(d0, mul_negi(d1));  // d0 - i d1
 }
 
-// Packed complex64 radix-8 (DIT from two radix-4): 28 FP instructions.
+// Packed complex64 radix-4 whose x2 arrives as t2 with a pending real factor
+// hs (a 45-degree twiddle h (1 -+ i) x = h t, t = x -+ i x): the factor rides
+// on the first butterfly (x0 +- hs t2 as two FFMA2), one instruction fewer
+// than scaling t2 first.
 template <bool INV>
-__device__ __forceinline__ void dft8_packed(float2* v)
+__device__ __forceinline__ void dft4_h(float2& x0, float2& x1, float2& t2, float2& x3, float hs)
+{
+    const float2 s0 = fma2(t2, make_float2(hs, hs), x0), d0 = fma2(t2, make_float2(-hs, -hs), x0);
+    const float2 s1 = add2(x1, x3), d1 = sub2(x1, x3);
+    x0 = add2(s0, s1);
+    t2 = sub2(s0, s1);
+    x1 = add2(d0, INV ? mul_i(d1) : mul_negi(d1));
+    x3 = add2(d0, INV ? mul_negi(d1) : mul_i(d1));
+}
+
+// Packed complex64 radix-8 (DIT from two radix-4): 26 FP instructions.
+// H: v[4] carries a pending real factor hs (see dft4_h).
+template <bool INV, bool H = false>
+__device__ __forceinline__ void dft8_packed(float2* v, float hs = 0.f)
 {
     float2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
     float2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
-    dft4<float, INV>(e0, e1, e2, e3);
+    if constexpr (H)
+        dft4_h<INV>(e0, e1, e2, e3, hs);
+    else
+        dft4<float, INV>(e0, e1, e2, e3);
     dft4<float, INV>(o0, o1, o2, o3);
     // twiddles with broadcast immediates: w8 = h (1 - i), w8^3 = -h (1 + i)
     const float h = 0.70710678118654752440f;
+    // the h scaling of the two 45-degree twiddles rides on the final
+    // butterflies (e +- h t as two FFMA2): 26 FP instructions
     if (!INV) {
-        o1 = mul2(add2(o1, mul_negi(o1)), make_float2(h, h));
-        o3 = mul2(add2(o3, mul_i(o3)), make_float2(-h, -h));
+        o1 = add2(o1, mul_negi(o1));
+        o3 = add2(o3, mul_i(o3));
         v[2] = add2(e2, mul_negi(o2));
         v[6] = add2(e2, mul_i(o2));
     } else {
-        o1 = mul2(add2(o1, mul_i(o1)), make_float2(h, h));
-        o3 = mul2(add2(o3, mul_negi(o3)), make_float2(-h, -h));
+        o1 = add2(o1, mul_i(o1));
+        o3 = add2(o3, mul_negi(o3));
         v[2] = add2(e2, mul_i(o2));
         v[6] = add2(e2, mul_negi(o2));
     }
+    const float2 hp = make_float2(h, h), hm = make_float2(-h, -h);
     v[0] = add2(e0, o0);
     v[4] = sub2(e0, o0);
-    v[1] = add2(e1, o1);
-    v[5] = sub2(e1, o1);
-    v[3] = add2(e3, o3);
-    v[7] = sub2(e3, o3);
+    v[1] = fma2(o1, hp, e1);
+    v[5] = fma2(o1, hm, e1);
+    v[3] = fma2(o3, hm, e3);
+    v[7] = fma2(o3, hp, e3);
 }
 
 // In-register DFT of size R: v[q] <- sum_r v[r] w_R^{rq}, w_R = exp(-+2 pi i/R).

@@ -81,10 +81,59 @@ struct Dft {
     // split P = P1 * P2: input r = P2 a + b, output q = c + P1 e
     static constexpr int P1 = P >= 16 ? 4 : 2;
     static constexpr int P2 = P / P1;
+    // 45-degree twiddles h (+-1 +- i) on the element that enters the next
+    // stage's first butterfly as x2 (B = P2 / 2) against an untwiddled x0:
+    // only the rotation t = x -+ i x is applied here, the real factor +-h
+    // rides on that butterfly (dft4_h), saving one instruction each
+    template <int B, int C>
+    static constexpr int k64_of()
+    {
+        return ((B * C) % P) * (64 / P);
+    }
+    template <int B, int C>
+    static constexpr bool h_fused()
+    {
+        return sizeof(T) == 4 && P >= 16 && B == P2 / 2 && k64_of<B, C>() % 16 == 8;
+    }
     template <int B, int C>
     __device__ __forceinline__ static void tw(T2* a)
     {
-        a[P2 * C + B] = cmul_const<T, P, B * C, INV>(a[P2 * C + B]);
+        if constexpr (h_fused<B, C>()) {
+            constexpr int k = k64_of<B, C>();
+            // forward: k = 8, 40 -> (1 - i), k = 24, 56 -> (1 + i); inverse swapped
+            constexpr bool minus_i = ((k == 8 || k == 40) != INV);
+            const float2 x = a[P2 * C + B];
+            a[P2 * C + B] = add2(x, minus_i ? mul_negi(x) : mul_i(x));
+        } else {
+            a[P2 * C + B] = cmul_const<T, P, B * C, INV>(a[P2 * C + B]);
+        }
+    }
+    // step 2 of group C: one transform of length P2 on a[P2 C ..), outputs to o[C + P1 e]
+    template <int C>
+    __device__ __forceinline__ static void group(T2* a, T2* o)
+    {
+        T2 s[P2];
+#pragma unroll
+        for (int i = 0; i < P2; ++i)
+            s[i] = a[P2 * C + i];
+        if constexpr (h_fused<P2 / 2, C>()) {
+            constexpr int k = k64_of<P2 / 2, C>();
+            constexpr float hs = (k == 8 || k == 56) ? 0.70710678118654752440f : -0.70710678118654752440f;
+            if constexpr (P2 == 4)
+                dft4_h<INV>(s[0], s[1], s[2], s[3], hs);
+            else
+                dft8_packed<INV, true>(s, hs);
+        } else {
+            Dft<T, P2, INV>::run(s);
+        }
+#pragma unroll
+        for (int e = 0; e < P2; ++e)
+            o[C + P1 * e] = s[e];
+    }
+    template <int... Cs>
+    __device__ __forceinline__ static void groups(T2* a, T2* o, std::integer_sequence<int, Cs...>)
+    {
+        (group<Cs>(a, o), ...);
     }
     __device__ __forceinline__ static void run(T2* a)
     {
@@ -98,6 +147,7 @@ struct Dft {
         } else if constexpr (P == 8) {
             dft_small<T, 8, INV>(a, nullptr, 0);
         } else {
+            static_assert(P2 == 4 || P2 == 8, "step 2 runs radix-4 or radix-8 groups");
             // step 1: P2 transforms of length P1 on stride-P2 subsequences
 #pragma unroll
             for (int b = 0; b < P2; ++b) {
@@ -114,17 +164,7 @@ struct Dft {
             twiddles(a, std::make_integer_sequence<int, P1 * P2>{});
             // step 2: P1 transforms of length P2 on contiguous groups
             T2 o[P];
-#pragma unroll
-            for (int c = 0; c < P1; ++c) {
-                T2 s[P2];
-#pragma unroll
-                for (int i = 0; i < P2; ++i)
-                    s[i] = a[P2 * c + i];
-                Dft<T, P2, INV>::run(s);
-#pragma unroll
-                for (int e = 0; e < P2; ++e)
-                    o[c + P1 * e] = s[e];
-            }
+            groups(a, o, std::make_integer_sequence<int, P1>{});
 #pragma unroll
             for (int q = 0; q < P; ++q)
                 a[q] = o[q];
