@@ -25,7 +25,8 @@ dt = torch.complex64 if info["precision"] == T.C64 else torch.complex128
 
 
 def timed(fn, reps):
-    fn()
+    for _ in range(3):  # the engine captures its launch graph on a repeated call
+        fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
