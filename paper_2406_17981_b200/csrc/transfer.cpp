@@ -16,6 +16,9 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -64,7 +67,13 @@ PinnedPool& pinned_pool()
 int transfer_threads(int64_t nchunks)
 {
     static const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-    return static_cast<int>(std::clamp<int64_t>(std::min<int64_t>(nchunks, hw), 1, 16));
+    // TSK_TRANSFER_THREADS overrides the worker count (A/B; default: host threads, at most 16)
+    static const int cap = [] {
+        const char* e = getenv("TSK_TRANSFER_THREADS");
+        const int v = e ? atoi(e) : 0;
+        return v > 0 ? std::min(v, 64) : 16;
+    }();
+    return static_cast<int>(std::clamp<int64_t>(std::min<int64_t>(nchunks, std::max(hw, cap > 16 ? cap : 0)), 1, cap));
 }
 
 // interleaved complex128 <-> operator precision, elements [0, n). The AVX2
@@ -241,7 +250,15 @@ void apply_host(const DeviceOperator& op, const double* v, double* y, const ts_p
         c->hy = DevBuf(vb, MEM_STAGING);
     }
     const int64_t count = op.s * op.m;
+    // TSK_DEBUG_TRANSFER=1: host wall clock of the three phases to stderr
+    static const bool dbg = [] {
+        const char* e = getenv("TSK_DEBUG_TRANSFER");
+        return e && e[0] == '1';
+    }();
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     host_transfer(0, op.device, const_cast<double*>(v), c->hx.p, op.es(), count);
+    const auto t1 = clk::now();
     cudaEvent_t e0, e1;
     cuda_check(cudaEventCreate(&e0), "event");
     cuda_check(cudaEventCreate(&e1), "event");
@@ -265,7 +282,16 @@ void apply_host(const DeviceOperator& op, const double* v, double* y, const ts_p
     cuda_check(cudaStreamSynchronize(c->st), "apply sync");
     float ms = 0.f;
     cuda_check(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+    const auto t2 = clk::now();
     host_transfer(1, op.device, y, c->hy.p, op.es(), count);
+    if (dbg) {
+        const auto ms_of = [](clk::time_point a, clk::time_point b) {
+            return std::chrono::duration<double, std::milli>(b - a).count();
+        };
+        fprintf(stderr, "ts_operator_apply: host->device %.1f ms, MVM %.1f ms, device->host %.1f ms (%.2f GB each way)\n",
+                ms_of(t0, t1), ms_of(t1, t2), ms_of(t2, clk::now()),
+                static_cast<double>(count) * static_cast<double>(op.es()) / 1e9);
+    }
     if (metrics) {
         if (op.is_embed)
             embed_counters(op, metrics);
