@@ -269,6 +269,9 @@ __device__ __forceinline__ void fft_one(typename cx<T>::t (&v)[R], typename cx<T
 #ifndef TSK_LEAF_LDEF
 #define TSK_LEAF_LDEF 0
 #endif
+#ifndef TSK_LEAF_XC
+#define TSK_LEAF_XC 0
+#endif
 // (Compressed storage only: with full storage the leaf reads each fiber's own
 // spectra from global memory and the extra registers of the TMEM chunks spill,
 // measured 3.83 -> 4.33 ms per launch at 512^3.)
@@ -551,7 +554,10 @@ __global__ void __launch_bounds__(G * 4 * M * (N / R), sizeof(T) == 4 && G * 4 *
     T2* xsu = stg0 + G * UM * LROW + (XS ? gi * CF * N : 0);  // this unit's rows
     uint32_t xphase = 0;
     auto issue_x = [&](int64_t tile_n) {
-        if (c != 0)  // warp-uniform: the component-0 warps issue for their fibers
+        // warp-uniform: one component's warps issue for their fibers.
+        // TSK_LEAF_XC: which one (A/B; with factorised signs the last
+        // component's warps have no per-fiber flips to apply)
+        if (c != (TSK_LEAF_XC < M ? TSK_LEAF_XC : 0))
             return;
         int64_t un = tile_n * G + gi;
         if (un >= units)
