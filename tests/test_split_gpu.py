@@ -324,8 +324,8 @@ np.savez({path!r}, **out)
 """
 
 
-def _run_with_env(env_var, cases):
-    """y for each case computed in a fresh process with env_var=1 (the
+def _run_with_env(env_var, cases, value="1"):
+    """y for each case computed in a fresh process with env_var=value (the
     kernel-selection switches are read once per process)."""
     import subprocess
     import sys
@@ -333,12 +333,25 @@ def _run_with_env(env_var, cases):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     with tempfile.TemporaryDirectory() as td:
         path = os.path.join(td, "y.npz")
-        env = dict(os.environ, **{env_var: "1"})
+        env = dict(os.environ, **{env_var: value})
         r = subprocess.run([sys.executable, "-c", _SUBPROC.format(root=root, cases=cases, path=path)],
                            env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         z = np.load(path)
         return [z[str(i)] for i in range(len(cases))]
+
+
+def test_host_apply_independent_of_transfer_worker_count():
+    # the ABI apply's pinned-chunk staging with 3 workers (TSK_TRANSFER_THREADS,
+    # fresh process; chunks then go round-robin over fewer slots) gives the
+    # bytes the default worker count gives; >= 64 MB so the chunked path runs
+    cases = [([64, 128, 513], T.SYM_GENERAL, T.C64, False)]
+    few = _run_with_env("TSK_TRANSFER_THREADS", cases, "3")
+    g = T.Generator.random(cases[0][0], 13, 1.0, T.SYM_GENERAL)
+    x = T.random_vector(cases[0][0], 13, 1.0)
+    assert x.nbytes >= 64 << 20
+    y = T.Operator.split_ex(T.BlockGenerator.from_scalar(g), precision=T.C64).apply(x)
+    assert np.array_equal(y, few[0])
 
 
 def test_fast_and_generic_agree():
