@@ -41,7 +41,11 @@ using wide::Tw;
 
 // N = 512 (R = 32, radix 32 x 16) or 256 (R = 16, radix 16 x 16); TF = 16
 // threads per column, W = 32 columns (256 B rows), 512 threads
-constexpr int TF = 16, W = 32, NT = TF * W, BOX_ROWS = 256;
+// rows per TMA box (<= 256; TSK_WTMA_BOX_ROWS: A/B of smaller boxes)
+#ifndef TSK_WTMA_BOX_ROWS
+#define TSK_WTMA_BOX_ROWS 256
+#endif
+constexpr int TF = 16, W = 32, NT = TF * W, BOX_ROWS = TSK_WTMA_BOX_ROWS;
 template <int N>
 struct Geo {
     static constexpr int R = N / TF;
@@ -136,6 +140,11 @@ struct Maps {
 // TSK_WTMA_LDEF=1 (A/B): the TMA tile loads carry an L2 evict-first policy
 #ifndef TSK_WTMA_LDEF
 #define TSK_WTMA_LDEF 0
+#endif
+// L2 promotion of the tile loads (CUtensorMapL2promotion: 0 none, 1 64 B, 2 128 B,
+// 3 256 B = one row segment; A/B)
+#ifndef TSK_WTMA_L2PROMO
+#define TSK_WTMA_L2PROMO 3
 #endif
 template <int MODE>
 __device__ __forceinline__ void st_out(float2* p, float2 v)
@@ -363,7 +372,7 @@ static bool make_map(CUtensorMap* m, const void* base, const tsk_axis& a)
     const cuuint32_t box[3] = {(cuuint32_t)W, (cuuint32_t)BOX_ROWS, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<void*>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, (CUtensorMapL2promotion)TSK_WTMA_L2PROMO,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
