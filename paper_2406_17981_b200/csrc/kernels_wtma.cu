@@ -45,7 +45,12 @@ using wide::Tw;
 #ifndef TSK_WTMA_BOX_ROWS
 #define TSK_WTMA_BOX_ROWS 256
 #endif
-constexpr int TF = 16, W = 32, NT = TF * W, BOX_ROWS = TSK_WTMA_BOX_ROWS;
+// TSK_WTMA_W (A/B): 16 columns (128 B rows, 256 threads) run two CTAs per SM
+#ifndef TSK_WTMA_W
+#define TSK_WTMA_W 32
+#endif
+constexpr int TF = 16, W = TSK_WTMA_W, NT = TF * W, BOX_ROWS = TSK_WTMA_BOX_ROWS;
+constexpr int CTAS_PER_SM = W == 32 ? 1 : 2;
 template <int N>
 struct Geo {
     static constexpr int R = N / TF;
@@ -56,7 +61,7 @@ struct Geo {
     static_assert(PL::NST == 2 && PL::radix(1) == 16, "two stages, radix R x 16");
     static constexpr size_t SMEM = TILE_BYTES + XROWS * W * 8 + (PL::TW + N) * 8;
     static constexpr int PW = 2 * R;   // TMEM words parked per thread
-    static constexpr int TCOLS = 4 * PW;  // four warps per lane quadrant
+    static constexpr int TCOLS = (NT / 128) * PW;  // NT / 128 warps per lane quadrant
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -156,7 +161,7 @@ __device__ __forceinline__ void st_out(float2* p, float2 v)
 }
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(NT, 1) k_wtma(tsk_axis p, const __grid_constant__ Maps maps)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_wtma(tsk_axis p, const __grid_constant__ Maps maps)
 {
     constexpr int R = Geo<N>::R;
     using PL = typename Geo<N>::PL;
@@ -422,7 +427,7 @@ static int launch(const tsk_axis& a, cudaStream_t st)
             return e;
         cached_dev = dev;
     }
-    const int64_t cap = sm_count();
+    const int64_t cap = (int64_t)sm_count() * CTAS_PER_SM;
     const int64_t grid = ntiles < cap ? ntiles : cap;
     const cudaError_t e = launch_pdl(pdl_for(a), kern, (unsigned)(grid > 0 ? grid : 1), NT, SMEM, st, a, maps);
     return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
