@@ -40,21 +40,30 @@ using wide::Plan;
 using wide::Tw;
 
 // N = 512 (R = 32, radix 32 x 16) or 256 (R = 16, radix 16 x 16); TF = 16
-// threads per column, W = 32 columns (256 B rows), 512 threads
+// threads per column
 // rows per TMA box (<= 256; TSK_WTMA_BOX_ROWS: A/B of smaller boxes)
 #ifndef TSK_WTMA_BOX_ROWS
 #define TSK_WTMA_BOX_ROWS 256
 #endif
-// TSK_WTMA_W (A/B): 16 columns (128 B rows, 256 threads) run two CTAs per SM
-#ifndef TSK_WTMA_W
-#define TSK_WTMA_W 32
+// W columns per tile: 32 (256 B rows, 512 threads, one CTA per SM) everywhere
+// except the merge pass at N = 256, which runs 16 columns (128 B rows, 256
+// threads) at two CTAs per SM — one CTA's stores then overlap the other's
+// transforms: K3 0.219 -> 0.201 ms (axis 1) and 0.224 -> 0.212 ms (axis 0) at
+// 256^3, while K1 there (0.205 -> 0.248 ms) and both passes at N = 512 (K1
+// 1.69 -> 2.14, K3 1.56 -> 1.87 ms) lose more DRAM efficiency to the shorter
+// row segments than the overlap returns (profiles/r02_ab_w16.txt).
+// TSK_WTMA_W3_256 (A/B): the merge pass's width at N = 256.
+#ifndef TSK_WTMA_W3_256
+#define TSK_WTMA_W3_256 16
 #endif
-constexpr int TF = 16, W = TSK_WTMA_W, NT = TF * W, BOX_ROWS = TSK_WTMA_BOX_ROWS;
-constexpr int CTAS_PER_SM = W == 32 ? 1 : 2;
-template <int N>
+constexpr int TF = 16, BOX_ROWS = TSK_WTMA_BOX_ROWS;
+template <int N, int W>
 struct Geo {
+    static_assert(W == 32 || W == 16, "256 B or 128 B rows");
+    static constexpr int NT = TF * W;
+    static constexpr int CTAS_PER_SM = W == 32 ? 1 : 2;
     static constexpr int R = N / TF;
-    static constexpr int TILE_BYTES = N * W * 8;  // 128 / 64 KB
+    static constexpr int TILE_BYTES = N * W * 8;  // 128 / 64 KB at W = 32
     // exchange buffer: half a tile at N = 512 (two rounds), a whole one below
     static constexpr int XROWS = N == 512 ? N / 2 : N;
     using PL = Plan<N, R>;
@@ -71,11 +80,11 @@ __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_
 // (rows t R + q) and reads the row pattern (rows t + 16 m); at N = 512 through
 // a buffer of half the tile: round 0 moves q < 16 / even m (rows with r % 32 <
 // 16), round 1 q >= 16 / odd m.
-template <int N, bool INV>
-__device__ __forceinline__ void fft_col(float2 (&v)[Geo<N>::R], float2* xb, const float2* tw, int t, int w)
+template <int N, int W, bool INV>
+__device__ __forceinline__ void fft_col(float2 (&v)[Geo<N, W>::R], float2* xb, const float2* tw, int t, int w)
 {
-    constexpr int R = Geo<N>::R;
-    using PL = typename Geo<N>::PL;
+    constexpr int R = Geo<N, W>::R;
+    using PL = typename Geo<N, W>::PL;
     Dft<float, R, INV>::run(v);
     if constexpr (N == 512) {
         float2 ev[R / 2];
@@ -160,15 +169,17 @@ __device__ __forceinline__ void st_out(float2* p, float2 v)
         *p = v;
 }
 
-template <int N, int MODE>
-__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_wtma(tsk_axis p, const __grid_constant__ Maps maps)
+template <int N, int MODE, int W>
+__global__ void __launch_bounds__(Geo<N, W>::NT, Geo<N, W>::CTAS_PER_SM)
+    k_wtma(tsk_axis p, const __grid_constant__ Maps maps)
 {
-    constexpr int R = Geo<N>::R;
-    using PL = typename Geo<N>::PL;
+    using GE = Geo<N, W>;
+    constexpr int R = GE::R, NT = GE::NT;
+    using PL = typename GE::PL;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float2* land = reinterpret_cast<float2*>(smem_raw);     // N x W landing tile
     float2* xb = land + N * W;                               // exchange rows
-    float2* tw = xb + Geo<N>::XROWS * W;                     // stage-B twiddles
+    float2* tw = xb + GE::XROWS * W;                     // stage-B twiddles
     float2* ph = tw + PL::TW;                                // split phase
     __shared__ __align__(8) uint64_t full;
     __shared__ uint32_t tmem_slot;
@@ -204,9 +215,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_wtma(tsk_axis p, const __gr
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (park) {
-        tbase = tmem_alloc(&tmem_slot, Geo<N>::TCOLS);
+        tbase = tmem_alloc(&tmem_slot, GE::TCOLS);
         const int warp = threadIdx.x / 32;
-        lane_base = tbase + ((uint32_t)(32 * (warp % 4)) << 16) + (uint32_t)(Geo<N>::PW * (warp / 4));
+        lane_base = tbase + ((uint32_t)(32 * (warp % 4)) << 16) + (uint32_t)(GE::PW * (warp / 4));
     } else {
         __syncthreads();
     }
@@ -231,7 +242,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_wtma(tsk_axis p, const __gr
         const int x = (int)(cb * W), z = (int)(c * p.outer + o);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full)),
-                     "r"(Geo<N>::TILE_BYTES)
+                     "r"(GE::TILE_BYTES)
                      : "memory");
 #if TSK_WTMA_LDEF
         uint64_t pol;
@@ -290,7 +301,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_wtma(tsk_axis p, const __gr
 #pragma unroll
                 for (int m = 0; m < R; ++m)
                     v[m] = cmul_tw<float, false>(v[m], load_tw<float>(ph + t + m * TF));
-                fft_col<N, false>(v, xb, tw, t, w);
+                fft_col<N, W, false>(v, xb, tw, t, w);
                 float2* dd = static_cast<float2*>(p.dst1) + base;
 #pragma unroll
                 for (int m = 0; m < R; ++m)
@@ -301,7 +312,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_wtma(tsk_axis p, const __gr
                 }
             }
             if (ue) {
-                fft_col<N, false>(v, xb, tw, t, w);
+                fft_col<N, W, false>(v, xb, tw, t, w);
                 float2* de = static_cast<float2*>(p.dst0) + base;
 #pragma unroll
                 for (int m = 0; m < R; ++m)
@@ -311,7 +322,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_wtma(tsk_axis p, const __gr
             float2* dst = static_cast<float2*>(p.dst0) + base;
             if (ue) {
                 take(v);
-                fft_col<N, true>(v, xb, tw, t, w);
+                fft_col<N, W, true>(v, xb, tw, t, w);
                 if (!uo) {
 #pragma unroll
                     for (int m = 0; m < R; ++m)
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_wtma(tsk_axis p, const __gr
                 tmem_park<float, R, false>(lane_base, v);  // waited before the restore
             }
             take(v);
-            fft_col<N, true>(v, xb, tw, t, w);
+            fft_col<N, W, true>(v, xb, tw, t, w);
 #pragma unroll
             for (int m = 0; m < R; ++m)
                 v[m] = cmul_tw<float, true>(v[m], load_tw<float>(ph + t + m * TF));
@@ -344,7 +355,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_wtma(tsk_axis p, const __gr
         }
     }
     if (park)
-        tmem_free(tbase, Geo<N>::TCOLS);
+        tmem_free(tbase, GE::TCOLS);
 }
 
 // ---- host side ------------------------------------------------------------
@@ -367,7 +378,7 @@ static EncodeFn encoder()
 }
 
 // [outer * ncomp][n][inner] complex64 tensor as 8-byte elements; box W x 256 x 1
-static bool make_map(CUtensorMap* m, const void* base, const tsk_axis& a)
+static bool make_map(CUtensorMap* m, const void* base, const tsk_axis& a, int W)
 {
     EncodeFn enc = encoder();
     if (!enc)
@@ -377,7 +388,7 @@ static bool make_map(CUtensorMap* m, const void* base, const tsk_axis& a)
     const cuuint32_t box[3] = {(cuuint32_t)W, (cuuint32_t)BOX_ROWS, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<void*>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, (CUtensorMapL2promotion)TSK_WTMA_L2PROMO,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, W == 32 ? (CUtensorMapL2promotion)TSK_WTMA_L2PROMO : CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -398,9 +409,10 @@ static int sm_count()
     return sms > 0 ? sms : 148;
 }
 
-template <int N, int MODE>
+template <int N, int MODE, int W>
 static int launch(const tsk_axis& a, cudaStream_t st)
 {
+    using GE = Geo<N, W>;
     if (a.inner % W != 0 || a.cstride != a.outer * N * a.inner || !(a.use_even || a.use_odd))
         return -1;
     const int64_t ntiles = a.outer * (a.inner / W) * a.ncomp;
@@ -411,14 +423,14 @@ static int launch(const tsk_axis& a, cudaStream_t st)
         return -1;
     Maps maps;
     std::memset(&maps, 0, sizeof(maps));
-    if (!make_map(&maps.m[0], in0, a))
+    if (!make_map(&maps.m[0], in0, a, W))
         return -1;
-    if (MODE == 1 && a.use_even && a.use_odd && !make_map(&maps.m[1], a.src1, a))
+    if (MODE == 1 && a.use_even && a.use_odd && !make_map(&maps.m[1], a.src1, a, W))
         return -1;
     if (MODE == 1 && !a.use_even)
         maps.m[1] = maps.m[0];
-    auto kern = k_wtma<N, MODE>;
-    constexpr size_t SMEM = Geo<N>::SMEM;
+    auto kern = k_wtma<N, MODE, W>;
+    constexpr size_t SMEM = GE::SMEM;
     static thread_local int cached_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -427,9 +439,9 @@ static int launch(const tsk_axis& a, cudaStream_t st)
             return e;
         cached_dev = dev;
     }
-    const int64_t cap = (int64_t)sm_count() * CTAS_PER_SM;
+    const int64_t cap = (int64_t)sm_count() * GE::CTAS_PER_SM;
     const int64_t grid = ntiles < cap ? ntiles : cap;
-    const cudaError_t e = launch_pdl(pdl_for(a), kern, (unsigned)(grid > 0 ? grid : 1), NT, SMEM, st, a, maps);
+    const cudaError_t e = launch_pdl(pdl_for(a), kern, (unsigned)(grid > 0 ? grid : 1), GE::NT, SMEM, st, a, maps);
     return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 
@@ -439,8 +451,8 @@ static int dispatch(const tsk_axis& a, cudaStream_t st)
     if (disabled() || !a.prec)
         return -1;
     switch (a.n) {
-    case 256: return launch<256, MODE>(a, st);
-    case 512: return launch<512, MODE>(a, st);
+    case 256: return launch<256, MODE, MODE == 1 ? TSK_WTMA_W3_256 : 32>(a, st);
+    case 512: return launch<512, MODE, 32>(a, st);
     default: return -1;
     }
 }
