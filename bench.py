@@ -685,8 +685,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("note: the timing rules ask for >= 3 warm-up steps", file=sys.stderr)
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        self_launch(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        self_launch(args)  # the reference arm is rank 0's host cores only: nothing to launch
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -419,9 +419,14 @@ static size_t tile_smem(const tsk_axis& a, int W, bool leaf)
     return b;
 }
 
+// Dynamic shared memory these kernels may use. The opt-in attribute is set to this
+// one value at every launch: a per-launch value would race between host threads
+// launching axes of different length (one lowers it under the other's launch).
+static constexpr size_t kSmemLimit = 200 * 1024;
+
 static int choose_w(const tsk_axis& a, bool leaf, int& W, size_t& smem)
 {
-    const size_t limit = 200 * 1024;
+    const size_t limit = kSmemLimit;
     const int64_t nfib = a.outer * a.inner;
     const int target = a.prec ? 4096 : 2048;  // complex elements per tile
     int w = (int)std::max<int64_t>(1, target / (a.ncomp * a.n));
@@ -450,7 +455,7 @@ static int launch(K kernel, size_t smem, int64_t ntiles, cudaStream_t st, const 
                   int W)
 {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+                                         (int)kSmemLimit);
     if (e != cudaSuccess)
         return (int)e;
     kernel<<<grid_for(ntiles), 256, smem, st>>>(a, W);
@@ -498,13 +503,13 @@ extern "C" int tsk_generic_leaf_pair(const tsk_axis* a, const tsk_spectra* sp, v
     cudaError_t e;
     if (a->prec) {
         e = cudaFuncSetAttribute(k_leaf_pair<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
+                                 (int)kSmemLimit);
         if (e != cudaSuccess)
             return (int)e;
         k_leaf_pair<float><<<grid_for(nt), 256, smem, st>>>(*a, *sp, W);
     } else {
         e = cudaFuncSetAttribute(k_leaf_pair<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
+                                 (int)kSmemLimit);
         if (e != cudaSuccess)
             return (int)e;
         k_leaf_pair<double><<<grid_for(nt), 256, smem, st>>>(*a, *sp, W);
