@@ -178,3 +178,28 @@ def test_different_operators_from_threads():
     for i in range(len(cases)):
         for r in range(reps):
             assert torch.equal(outs[i][r], serial[i]), (cases[i], r)
+
+
+def test_large_host_abi_applies_from_threads():
+    # >= 64 MB of host complex128 per call: the chunked pinned-staging transfer (csrc/transfer.cpp,
+    # worker threads, shared pinned-slot pool) entered from two threads at once
+    levels = [64, 128, 513]
+    g = T.Generator.random(levels, 29, 1.0, T.SYM_GENERAL)
+    op = T.Operator.split_ex(T.BlockGenerator.from_scalar(g), precision=T.C64)
+    vs = [T.random_vector(levels, 29 + i, 1.0) for i in range(2)]
+    assert vs[0].nbytes >= 64 << 20
+    serial = [op.apply(v) for v in vs]
+    got = [[None] * 2 for _ in vs]
+    start = threading.Barrier(len(vs))
+
+    def worker(i):
+        def f():
+            start.wait()
+            for r in range(2):
+                got[i][r] = op.apply(vs[i])
+        return f
+
+    _run_threads([worker(i) for i in range(len(vs))])
+    for i in range(len(vs)):
+        for r in range(2):
+            assert np.array_equal(got[i][r], serial[i]), (i, r)
