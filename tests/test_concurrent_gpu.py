@@ -203,3 +203,26 @@ def test_large_host_abi_applies_from_threads():
     for i in range(len(vs)):
         for r in range(2):
             assert np.array_equal(got[i][r], serial[i]), (i, r)
+
+
+def test_embedding_engine_applies_from_threads():
+    # the full-embedding engine (ref proj/src/core/engine_embed.cpp:113-168) shares the apply contexts
+    levels = [24, 20, 18]
+    g = T.Generator.random(levels, 3, 1.0, T.SYM_GENERAL)
+    op = T.Operator.embed(g)
+    vs = [T.random_vector(levels, 400 + i, 1.0) for i in range(3)]
+    serial = [op.apply(v) for v in vs]
+    got = [[None] * 4 for _ in vs]
+    start = threading.Barrier(len(vs))
+
+    def worker(i):
+        def f():
+            start.wait()
+            for r in range(4):
+                got[i][r] = op.apply(vs[i])
+        return f
+
+    _run_threads([worker(i) for i in range(len(vs))])
+    for i in range(len(vs)):
+        for r in range(4):
+            assert np.array_equal(got[i][r], serial[i]), (i, r)
