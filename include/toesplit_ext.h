@@ -94,7 +94,8 @@ ts_status ts_operator_create_embed_ex(const ts_block_generator* g, const ts_spli
                                       ts_operator** out);
 
 /* y = T x on device memory: x, y hold m components of prod(levels) elements of
- * the operator's precision (float2 / double2), may not alias; stream is a
+ * the operator's precision (float2 / double2), 16-byte aligned (else
+ * TS_ERR_INVALID_ARGUMENT), may not alias; stream is a
  * cudaStream_t (NULL = legacy default stream). Asynchronous: returns after
  * enqueueing; metrics (nullable) carries counters, apply_ns = 0. Workspace is
  * stream-ordered per call, so concurrent calls on different streams are safe.

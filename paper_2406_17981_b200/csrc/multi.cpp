@@ -419,6 +419,8 @@ void apply_device_comm(const DeviceOperator& op, Comm* comm, const void* x, void
         fail(TS_ERR_INVALID_ARGUMENT, "invalid root rank");
     if (!x || !y || x == y)
         fail(TS_ERR_INVALID_ARGUMENT, "x and y must be distinct device buffers");
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)
+        fail(TS_ERR_INVALID_ARGUMENT, "x and y must be 16-byte aligned device pointers");
     const NcclApi& api = nccl();
     std::lock_guard<std::mutex> lk(comm->mu);
     DeviceGuard guard(op.device);

@@ -469,6 +469,10 @@ static void check_vectors(const DeviceOperator& op, const void* x, const void* y
         fail(TS_ERR_INVALID_ARGUMENT, "null argument");
     if (nrhs < 1)
         fail(TS_ERR_INVALID_ARGUMENT, "nrhs must be >= 1");
+    // the fast passes move 16-byte vectors and bulk-copy rows (cp.async.bulk / TMA):
+    // a base pointer off that alignment would fault inside a kernel
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)
+        fail(TS_ERR_INVALID_ARGUMENT, "x and y must be 16-byte aligned device pointers");
     const size_t vb = op.vec_bytes() * static_cast<size_t>(nrhs);
     const char* xb = static_cast<const char*>(x);
     const char* yb = static_cast<const char*>(y);

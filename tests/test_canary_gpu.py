@@ -62,3 +62,26 @@ def test_no_write_outside_y(levels, kind, prec):
         assert torch.equal(x, x0), "x modified"
         assert torch.equal(y, plain)
         assert bool(torch.isfinite(torch.view_as_real(y)).all())
+
+
+def test_misaligned_device_pointers_are_rejected_not_faulted():
+    # the fast passes use 16-byte vector accesses and bulk row copies: an x or y that is only
+    # 8-byte aligned (a complex64 view at an odd element offset) is refused at the ABI
+    # (TS_ERR_INVALID_ARGUMENT) instead of faulting in a kernel; aligned views work
+    import torch
+
+    levels = [8, 16, 512]
+    op = T.Operator.split_ex(T.BlockGenerator.dyadic(levels), precision=T.C64)
+    n = 3 * int(np.prod(levels))
+    x = torch.randn(n + 8, dtype=torch.complex64, device="cuda")
+    y = torch.zeros(n + 8, dtype=torch.complex64, device="cuda")
+    ref = torch.empty(n, dtype=torch.complex64, device="cuda")
+    op.apply_device(x[2:2 + n], ref)
+    for ox, oy in ((3, 0), (2, 1), (3, 5)):
+        with pytest.raises(T.TsError) as e:
+            op.apply_device(x[ox:ox + n], y[oy:oy + n])
+        assert e.value.code == T.TS_ERR_INVALID_ARGUMENT
+    op.apply_device(x[2:2 + n], y[4:4 + n])
+    torch.cuda.synchronize()
+    assert torch.equal(y[4:4 + n], ref)
+    assert float(y[:4].abs().sum()) == 0 and float(y[4 + n:].abs().sum()) == 0
